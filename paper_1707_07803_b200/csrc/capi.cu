@@ -1,0 +1,356 @@
+// extern "C" boundary (include/mpo_b200.h): handles, argument validation,
+// exception -> status-code mapping.  See the header for the reference
+// functions each entry point replaces.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "convert.cuh"
+#include "kernels.cuh"
+#include "mpo_b200.h"
+#include "tnrsvd.cuh"
+
+#define MPO_API extern "C" __attribute__((visibility("default")))
+
+namespace mpob {
+unsigned long long g_launches = 0;
+}
+
+struct mpo_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+};
+
+struct mpo_dev {
+  mpob::Cores cores;
+};
+
+struct mpo_conv {
+  mpob::ConvLocal c;
+  std::vector<int64_t> rf, cf;
+  int64_t nrb = 1;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(mpo_ctx* ctx, F&& f) {
+  try {
+    if (ctx) CK(cudaSetDevice(ctx->device));
+    f();
+    return MPO_OK;
+  } catch (const mpob::ValueError& e) {
+    g_err = e.what();
+    return MPO_EVALUE;
+  } catch (const mpob::OutOfMemory& e) {
+    g_err = e.what();
+    return MPO_ENOMEM;
+  } catch (const mpob::CudaError& e) {
+    g_err = e.what();
+    return MPO_ECUDA;
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    return MPO_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MPO_EINTERNAL;
+  }
+}
+
+void need(bool ok, const char* msg) {
+  if (!ok) throw mpob::ValueError(msg);
+}
+
+cudaMemcpyKind kind_in(int from_host) {
+  return from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+}
+cudaMemcpyKind kind_out(int to_host) {
+  return to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+}
+
+mpo_dev* wrap(mpob::Cores&& c) {
+  auto* m = new mpo_dev;
+  m->cores = std::move(c);
+  return m;
+}
+
+}  // namespace
+
+MPO_API const char* mpo_b200_last_error(void) { return g_err.c_str(); }
+MPO_API int mpo_b200_abi_version(void) { return 1; }
+MPO_API unsigned long long mpo_b200_launch_count(void) { return mpob::g_launches; }
+
+MPO_API int mpo_ctx_create(int device, void* stream, mpo_ctx** out) {
+  return guarded(nullptr, [&] {
+    need(out != nullptr, "null output pointer");
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    need(device >= 0 && device < n, "invalid CUDA device");
+    CK(cudaSetDevice(device));
+    // keep freed pool blocks cached: the sweeps allocate/free per bond
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = ~0ull;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    auto* c = new mpo_ctx;
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(stream);
+    *out = c;
+  });
+}
+
+MPO_API int mpo_ctx_set_stream(mpo_ctx* ctx, void* stream) {
+  return guarded(ctx, [&] { ctx->stream = static_cast<cudaStream_t>(stream); });
+}
+
+MPO_API int mpo_ctx_synchronize(mpo_ctx* ctx) {
+  return guarded(ctx, [&] { CK(cudaStreamSynchronize(ctx->stream)); });
+}
+
+MPO_API int mpo_ctx_destroy(mpo_ctx* ctx) {
+  delete ctx;
+  return MPO_OK;
+}
+
+// ---- MPO handles -------------------------------------------------------------
+MPO_API int mpo_dev_create(mpo_ctx* ctx, int d, const int64_t* shapes, const double* const* cores,
+                           int from_host, mpo_dev** out) {
+  return guarded(ctx, [&] {
+    need(d >= 1, "an MPO needs at least one core");
+    mpob::Cores cs;
+    for (int k = 0; k < d; ++k) {
+      const int64_t* s = shapes + 4 * k;
+      for (int q = 0; q < 4; ++q)
+        if (s[q] < 1) throw mpob::ValueError("core " + std::to_string(k) + " has empty extent");
+      mpob::Core c = mpob::make_core(ctx->stream, s[0], s[1], s[2], s[3]);
+      CK(cudaMemcpyAsync(c.p(), cores[k], sizeof(double) * c.size(), kind_in(from_host),
+                         ctx->stream));
+      cs.push_back(std::move(c));
+    }
+    mpob::validate_chain(cs);
+    *out = wrap(std::move(cs));
+  });
+}
+
+MPO_API int mpo_dev_num_cores(const mpo_dev* m, int* d) {
+  *d = (int)m->cores.size();
+  return MPO_OK;
+}
+
+MPO_API int mpo_dev_shapes(const mpo_dev* m, int64_t* shapes) {
+  for (size_t k = 0; k < m->cores.size(); ++k) {
+    const auto& c = m->cores[k];
+    shapes[4 * k] = c.R; shapes[4 * k + 1] = c.I; shapes[4 * k + 2] = c.J; shapes[4 * k + 3] = c.S;
+  }
+  return MPO_OK;
+}
+
+MPO_API int mpo_dev_core_ptr(const mpo_dev* m, int k, const double** p) {
+  if (k < 0 || k >= (int)m->cores.size()) { g_err = "core index out of range"; return MPO_EVALUE; }
+  *p = m->cores[k].p();
+  return MPO_OK;
+}
+
+MPO_API int mpo_dev_copy_core(mpo_ctx* ctx, const mpo_dev* m, int k, double* dst, int to_host) {
+  return guarded(ctx, [&] {
+    need(k >= 0 && k < (int)m->cores.size(), "core index out of range");
+    const auto& c = m->cores[k];
+    CK(cudaMemcpyAsync(dst, c.p(), sizeof(double) * c.size(), kind_out(to_host), ctx->stream));
+    if (to_host) CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+MPO_API int mpo_dev_free(mpo_dev* m) {
+  delete m;
+  return MPO_OK;
+}
+
+// ---- TNrSVD stages -----------------------------------------------------------
+MPO_API int mpo_matmul(mpo_ctx* ctx, const mpo_dev* a, int ta, const mpo_dev* b, int tb,
+                       mpo_dev** out) {
+  return guarded(ctx, [&] { *out = wrap(mpob::matmul(ctx->stream, a->cores, ta, b->cores, tb)); });
+}
+
+MPO_API int mpo_transpose(mpo_ctx* ctx, const mpo_dev* a, mpo_dev** out) {
+  return guarded(ctx, [&] { *out = wrap(mpob::transpose(ctx->stream, a->cores)); });
+}
+
+MPO_API int mpo_merge_leading_cores(mpo_ctx* ctx, const mpo_dev* m, int count, mpo_dev** out) {
+  return guarded(ctx, [&] { *out = wrap(mpob::merge_leading(ctx->stream, m->cores, count)); });
+}
+
+MPO_API int mpo_qr(mpo_ctx* ctx, const mpo_dev* y, double tol, int has_tol, mpo_dev** q,
+                   double* r_host) {
+  return guarded(ctx, [&] {
+    mpob::DBuf<double> r;
+    mpob::Cores qc = mpob::qr(ctx->stream, y->cores, has_tol != 0, tol, &r);
+    if (r_host && r.size())
+      CK(cudaMemcpyAsync(r_host, r.get(), sizeof(double) * r.size(), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *q = wrap(std::move(qc));
+  });
+}
+
+MPO_API int mpo_svd(mpo_ctx* ctx, const mpo_dev* b, double tol, int has_tol, double* w_host,
+                    double* s_host, mpo_dev** v) {
+  return guarded(ctx, [&] {
+    mpob::DBuf<double> w, s;
+    mpob::Cores vc = mpob::svd(ctx->stream, b->cores, has_tol != 0, tol, w, s);
+    if (w_host)
+      CK(cudaMemcpyAsync(w_host, w.get(), sizeof(double) * w.size(), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    if (s_host)
+      CK(cudaMemcpyAsync(s_host, s.get(), sizeof(double) * s.size(), cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *v = wrap(std::move(vc));
+  });
+}
+
+MPO_API int mpo_subspace_iteration(mpo_ctx* ctx, const mpo_dev* a, const mpo_dev* o, int q,
+                                   double tol, int has_tol, mpo_dev** out) {
+  return guarded(ctx, [&] {
+    *out = wrap(mpob::subspace_iteration(ctx->stream, a->cores, o->cores, q, has_tol != 0, tol));
+  });
+}
+
+MPO_API int mpo_tnrsvd(mpo_ctx* ctx, const mpo_dev* am, const mpo_dev* o, int k_target, int q,
+                       double tol, int has_tol, mpo_dev** u, double* s_host, mpo_dev** v) {
+  return guarded(ctx, [&] {
+    mpob::Cores uc, vc;
+    std::vector<double> s;
+    mpob::tnrsvd(ctx->stream, am->cores, o->cores, k_target, q, has_tol != 0, tol, uc, s, vc);
+    std::memcpy(s_host, s.data(), sizeof(double) * s.size());
+    *u = wrap(std::move(uc));
+    *v = wrap(std::move(vc));
+  });
+}
+
+MPO_API int mpo_round(mpo_ctx* ctx, const mpo_dev* m, double rel_tol, mpo_dev** out) {
+  return guarded(ctx, [&] { *out = wrap(mpob::round_cores(ctx->stream, m->cores, rel_tol)); });
+}
+
+MPO_API int mpo_add(mpo_ctx* ctx, const mpo_dev* a, const mpo_dev* b, mpo_dev** out) {
+  return guarded(ctx, [&] { *out = wrap(mpob::add(ctx->stream, a->cores, b->cores)); });
+}
+
+// ---- conversion --------------------------------------------------------------
+MPO_API int mpo_sparse_convert(mpo_ctx* ctx, const int64_t* row1, const int64_t* col1,
+                               const double* val, int64_t n, int from_host, int d,
+                               const int64_t* rf, const int64_t* cf, mpo_conv** out) {
+  return guarded(ctx, [&] {
+    need(d >= 1, "factor lists must be non-empty and equal length");
+    need(n >= 0, "negative entry count");
+    auto* c = new mpo_conv;
+    try {
+      c->rf.assign(rf, rf + d);
+      c->cf.assign(cf, cf + d);
+      int64_t ncb = 1;
+      for (int q = 1; q < d; ++q) { c->nrb *= rf[q]; ncb *= cf[q]; }
+      const cudaStream_t st = ctx->stream;
+      const int64_t* r = row1;
+      const int64_t* cc = col1;
+      const double* v = val;
+      mpob::DBuf<int64_t> hr, hc;
+      mpob::DBuf<double> hv;
+      if (from_host && n > 0) {
+        hr.alloc(n, st); hc.alloc(n, st); hv.alloc(n, st);
+        CK(cudaMemcpyAsync(hr.get(), row1, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(hc.get(), col1, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(hv.get(), val, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        r = hr.get(); cc = hc.get(); v = hv.get();
+      }
+      c->c = mpob::convert_local(st, r, cc, v, n, rf[0], cf[0], c->nrb, ncb);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+MPO_API int mpo_conv_info(const mpo_conv* c, int64_t* nkept, int64_t* rank) {
+  if (nkept) *nkept = c->c.nkept;
+  if (rank) *rank = c->c.rank;
+  return MPO_OK;
+}
+
+MPO_API int mpo_conv_copy(mpo_ctx* ctx, const mpo_conv* c, int64_t* i1, int64_t* j1, int64_t* ti,
+                          double* values, int64_t* uniq, int to_host) {
+  return guarded(ctx, [&] {
+    const cudaStream_t st = ctx->stream;
+    const int64_t n = c->c.nkept, r = c->c.rank;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) CK(cudaMemcpyAsync(dst, src, bytes, kind_out(to_host), st));
+    };
+    cp(i1, c->c.i1.get(), sizeof(int64_t) * n);
+    cp(j1, c->c.j1.get(), sizeof(int64_t) * n);
+    cp(ti, c->c.ti.get(), sizeof(int64_t) * n);
+    cp(values, c->c.values.get(), sizeof(double) * n);
+    cp(uniq, c->c.uniq.get(), sizeof(int64_t) * r);
+    if (to_host) CK(cudaStreamSynchronize(st));
+  });
+}
+
+MPO_API int mpo_conv_level(mpo_ctx* ctx, const mpo_conv* c, int level, int64_t* rowd,
+                           int64_t* cold, int to_host) {
+  return guarded(ctx, [&] {
+    need(level >= 1 && level < (int)c->rf.size(), "level out of range");
+    const cudaStream_t st = ctx->stream;
+    const int64_t r = c->c.rank;
+    if (!to_host) {
+      mpob::level_digits(st, c->c.uniq.get(), r, c->nrb, c->rf, c->cf, level, rowd, cold);
+      return;
+    }
+    mpob::DBuf<int64_t> a(r, st), b(r, st);
+    mpob::level_digits(st, c->c.uniq.get(), r, c->nrb, c->rf, c->cf, level, a.get(), b.get());
+    if (r) {
+      CK(cudaMemcpyAsync(rowd, a.get(), sizeof(int64_t) * r, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(cold, b.get(), sizeof(int64_t) * r, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+MPO_API int mpo_conv_dense_core(mpo_ctx* ctx, const mpo_conv* c, int level, double* dst,
+                                int to_host) {
+  return guarded(ctx, [&] {
+    const int d = (int)c->rf.size();
+    need(level >= 0 && level < d, "level out of range");
+    need(c->c.rank >= 1, "no blocks");
+    const cudaStream_t st = ctx->stream;
+    const int64_t r = c->c.rank;
+    int64_t sz = (level == 0) ? c->rf[0] * c->cf[0] * r
+                              : r * c->rf[level] * c->cf[level] * (level == d - 1 ? 1 : r);
+    if (!to_host) {
+      mpob::conv_dense_core(st, c->c, c->rf, c->cf, level, dst);
+      return;
+    }
+    mpob::DBuf<double> tmp(sz, st);
+    mpob::conv_dense_core(st, c->c, c->rf, c->cf, level, tmp.get());
+    CK(cudaMemcpyAsync(dst, tmp.get(), sizeof(double) * sz, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+MPO_API int mpo_conv_free(mpo_conv* c) {
+  delete c;
+  return MPO_OK;
+}
+
+MPO_API int mpo_keys_unique(mpo_ctx* ctx, const int64_t* keys, int64_t n, int64_t max_key,
+                            int64_t* out, int64_t* nuniq) {
+  return guarded(ctx, [&] { *nuniq = mpob::keys_unique(ctx->stream, keys, n, max_key, out); });
+}
+
+MPO_API int mpo_keys_lookup(mpo_ctx* ctx, const int64_t* table, int64_t ntab, const int64_t* q,
+                            int64_t nq, int64_t* out) {
+  return guarded(ctx, [&] { mpob::keys_lookup(ctx->stream, table, ntab, q, nq, out); });
+}
+
+MPO_API int mpo_remap_ids(mpo_ctx* ctx, const int64_t* map, int64_t* ti, int64_t n) {
+  return guarded(ctx, [&] { mpob::remap_ids(ctx->stream, map, ti, n); });
+}

@@ -1,0 +1,88 @@
+// Shared plumbing for the sm_100a kernels: error handling, stream-ordered
+// device buffers, small device helpers.  All matrices are FP64 and
+// column-major ("F order", first index fastest), the layout of the
+// reference's cores (mpo.py:17-23) and of every unfolding the sweeps use.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace mpob {
+
+// A precondition failure: maps to the reference's ValueError.
+struct ValueError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+// A CUDA failure: maps to RuntimeError.
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+// Device allocation failure: maps to MemoryError (numpy's on the CPU path).
+struct OutOfMemory : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s failed at %s:%d: %s", what, file, line, cudaGetErrorString(e));
+  if (e == cudaErrorMemoryAllocation) throw OutOfMemory(buf);
+  throw CudaError(buf);
+}
+#define CK(x) ::mpob::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH() ::mpob::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Stream-ordered device buffer (cudaMallocAsync from the device's default
+// pool, whose release threshold the context raises so freed blocks are
+// recycled instead of returned to the driver between sweeps).
+template <typename T>
+class DBuf {
+ public:
+  DBuf() = default;
+  DBuf(size_t n, cudaStream_t s) { alloc(n, s); }
+  ~DBuf() { reset(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) { o.p_ = nullptr; o.n_ = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { reset(); p_ = o.p_; n_ = o.n_; s_ = o.s_; o.p_ = nullptr; o.n_ = 0; }
+    return *this;
+  }
+  void alloc(size_t n, cudaStream_t s) {
+    reset();
+    s_ = s;
+    n_ = n;
+    if (n) {
+      void* p = nullptr;
+      CK(cudaMallocAsync(&p, n * sizeof(T), s));
+      p_ = static_cast<T*>(p);
+    }
+  }
+  void reset() {
+    if (p_) cudaFreeAsync(p_, s_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  cudaStream_t stream() const { return s_; }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+  cudaStream_t s_ = nullptr;
+};
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Count of our own kernel launches (reported by bench.py as gpu_launches).
+extern unsigned long long g_launches;
+inline void note_launch(int n = 1) { g_launches += (unsigned long long)n; }
+
+}  // namespace mpob

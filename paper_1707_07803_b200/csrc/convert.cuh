@@ -1,0 +1,42 @@
+// Sparse -> MPO conversion structure (convert.cu).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace mpob {
+
+// Result of the single-device conversion of one nnz shard (sparse.py:234-250):
+// per kept nonzero (input order) i1, j1, values and block id ti; the sorted
+// unique block keys uniq (key = br + nrb * bc).
+struct ConvLocal {
+  DBuf<int64_t> i1, j1, ti, uniq;
+  DBuf<double> values;
+  int64_t nkept = 0;
+  int64_t rank = 0;
+};
+
+ConvLocal convert_local(cudaStream_t st, const int64_t* row1, const int64_t* col1,
+                        const double* val, int64_t n, int64_t I1, int64_t J1, int64_t nrb,
+                        int64_t ncb);
+void level_digits(cudaStream_t st, const int64_t* uniq, int64_t rank, int64_t nrb,
+                  const std::vector<int64_t>& rf, const std::vector<int64_t>& cf, int level,
+                  int64_t* rowd, int64_t* cold);
+void exclusive_scan_u32(cudaStream_t st, const unsigned* in, int64_t n, int64_t* out,
+                        int64_t* total_dev);
+int key_bits(uint64_t max_key);
+void radix_sort_pairs(cudaStream_t st, uint64_t* key, unsigned* pay, int64_t n, int bits,
+                      uint64_t* key_tmp, unsigned* pay_tmp, bool& result_in_tmp);
+
+}  // namespace mpob
+
+namespace mpob {
+void conv_dense_core(cudaStream_t st, const ConvLocal& c, const std::vector<int64_t>& rf,
+                     const std::vector<int64_t>& cf, int level, double* out);
+int64_t keys_unique(cudaStream_t st, const int64_t* keys, int64_t n, int64_t max_key,
+                    int64_t* out);
+void keys_lookup(cudaStream_t st, const int64_t* table, int64_t ntab, const int64_t* q,
+                 int64_t nq, int64_t* out);
+void remap_ids(cudaStream_t st, const int64_t* map, int64_t* ti, int64_t n);
+}  // namespace mpob

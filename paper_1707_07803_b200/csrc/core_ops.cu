@@ -1,0 +1,277 @@
+// Elementwise / data-movement kernels of the TNrSVD path: the per-core MPO
+// product (rsvd.py:62-79), F-order permutations (the reshape/transpose
+// bookkeeping of rsvd.py:97, :159-160, :192), copies, scaling and the
+// deterministic Frobenius norm of rsvd.py:123.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mpob {
+
+namespace {
+
+inline int grid_for(int64_t n, int threads = 256) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, threads), 148 * 16));
+}
+
+__global__ void scale_kernel(int64_t m, int64_t n, double alpha, double* C, int64_t ldc,
+                             int64_t batch, int64_t sC) {
+  const int64_t total = m * n * batch;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = idx / (m * n), r = idx % (m * n);
+    double* p = C + b * sC + (r % m) + (r / m) * ldc;
+    *p = alpha == 0.0 ? 0.0 : alpha * *p;
+  }
+}
+
+__global__ void copy_kernel(int64_t m, int64_t n, const double* __restrict__ A, int64_t lda,
+                            double* __restrict__ B, int64_t ldb) {
+  const int64_t total = m * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = idx % m, j = idx / m;
+    B[i + j * ldb] = A[i + j * lda];
+  }
+}
+
+__global__ void identity_kernel(int64_t m, int64_t n, double* A, int64_t lda) {
+  const int64_t total = m * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = idx % m, j = idx / m;
+    A[i + j * lda] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+struct PermArgs {
+  int rank;
+  int64_t odims[6];    // output extents
+  int64_t istride[6];  // input stride of the input axis feeding output axis q
+  int64_t total;
+};
+
+__global__ void permute_kernel(const double* __restrict__ in, double* __restrict__ out,
+                               PermArgs a) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < a.total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = idx, off = 0;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      if (q < a.rank) {
+        int64_t c = rem % a.odims[q];
+        rem /= a.odims[q];
+        off += c * a.istride[q];
+      }
+    }
+    out[idx] = in[off];
+  }
+}
+
+// N[a + Ra*c, i, k, b + Sa*d] = sum_j A[a,i,j,b] * B[c,j,k,d]; one output
+// element per thread (write-bound: 2J flops per 8-byte store), A and B
+// cores are small and stay in L1/L2.
+struct ProdArgs {
+  const double* A;
+  const double* B;
+  double* N;
+  int64_t Ra, I, J, Sa, Rb, K, Sb;
+  int64_t aI, aJ, aS;  // element strides of A's logical axes i, j, b (a stride 1)
+  int64_t bJ, bK, bS;  // element strides of B's logical axes j, k, d (c stride 1)
+  int64_t total;
+};
+
+__global__ void core_product_kernel(ProdArgs p) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < p.total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = idx;
+    const int64_t a = r % p.Ra; r /= p.Ra;
+    const int64_t c = r % p.Rb; r /= p.Rb;
+    const int64_t i = r % p.I; r /= p.I;
+    const int64_t k = r % p.K; r /= p.K;
+    const int64_t b = r % p.Sa; r /= p.Sa;
+    const int64_t d = r;
+    const double* pa = p.A + a + i * p.aI + b * p.aS;
+    const double* pb = p.B + c + k * p.bK + d * p.bS;
+    double s = 0.0;
+    for (int64_t j = 0; j < p.J; ++j) s = fma(pa[j * p.aJ], pb[j * p.bJ], s);
+    p.N[idx] = s;
+  }
+}
+
+// deterministic sum of squares: per-block partials then one block
+__global__ void sumsq_partial(const double* __restrict__ x, int64_t n, double* part) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    s = fma(x[i], x[i], s);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void sumsq_final(const double* part, int n, double* out) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sqrt(sh[0]);
+}
+
+}  // namespace
+
+void scale_matrix(cudaStream_t st, int64_t m, int64_t n, double alpha, double* C, int64_t ldc,
+                  int64_t batch, int64_t sC) {
+  if (m <= 0 || n <= 0 || batch <= 0 || alpha == 1.0) return;
+  scale_kernel<<<grid_for(m * n * batch), 256, 0, st>>>(m, n, alpha, C, ldc, batch, sC);
+  CK_LAUNCH();
+  note_launch();
+}
+
+void copy_matrix(cudaStream_t st, int64_t m, int64_t n, const double* A, int64_t lda, double* B,
+                 int64_t ldb) {
+  if (m <= 0 || n <= 0) return;
+  if (lda == m && ldb == m) {
+    CK(cudaMemcpyAsync(B, A, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  copy_kernel<<<grid_for(m * n), 256, 0, st>>>(m, n, A, lda, B, ldb);
+  CK_LAUNCH();
+  note_launch();
+}
+
+void set_identity(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda) {
+  if (m <= 0 || n <= 0) return;
+  identity_kernel<<<grid_for(m * n), 256, 0, st>>>(m, n, A, lda);
+  CK_LAUNCH();
+  note_launch();
+}
+
+void fill_zero(cudaStream_t st, double* p, int64_t n) {
+  if (n > 0) CK(cudaMemsetAsync(p, 0, sizeof(double) * n, st));
+}
+
+void permute(cudaStream_t st, const double* in, double* out, int rank, const int64_t* dims,
+             const int* perm) {
+  if (rank < 1 || rank > 6) throw ValueError("permute rank must be 1..6");
+  int64_t istr[6];
+  int64_t s = 1;
+  for (int q = 0; q < rank; ++q) { istr[q] = s; s *= dims[q]; }
+  PermArgs a;
+  a.rank = rank;
+  a.total = s;
+  bool identity = true;
+  for (int q = 0; q < 6; ++q) { a.odims[q] = 1; a.istride[q] = 0; }
+  for (int q = 0; q < rank; ++q) {
+    a.odims[q] = dims[perm[q]];
+    a.istride[q] = istr[perm[q]];
+    if (perm[q] != q && dims[perm[q]] != 1) identity = false;
+  }
+  if (s == 0) return;
+  if (identity) {
+    // only unit axes move: the memory image is unchanged
+    CK(cudaMemcpyAsync(out, in, sizeof(double) * s, cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  permute_kernel<<<grid_for(s), 256, 0, st>>>(in, out, a);
+  CK_LAUNCH();
+  note_launch();
+}
+
+void frob_norm(cudaStream_t st, const double* x, int64_t n, double* out_dev) {
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 296));
+  DBuf<double> part(blocks, st);
+  sumsq_partial<<<blocks, 256, 0, st>>>(x, n, part.get());
+  CK_LAUNCH();
+  sumsq_final<<<1, 256, 0, st>>>(part.get(), blocks, out_dev);
+  CK_LAUNCH();
+  note_launch(2);
+}
+
+void core_product(cudaStream_t st, const CoreView& a, const CoreView& b, double* out) {
+  if (a.J != b.I) throw ValueError("inner dims differ per core");
+  ProdArgs p;
+  p.A = a.p;
+  p.B = b.p;
+  p.N = out;
+  p.Ra = a.R; p.I = a.I; p.J = a.J; p.Sa = a.S;
+  p.Rb = b.R; p.K = b.J; p.Sb = b.S;
+  // A physical (R, I, J, S) or (R, J, I, S) when transposed
+  if (!a.trans) { p.aI = a.R; p.aJ = a.R * a.I; }
+  else { p.aJ = a.R; p.aI = a.R * a.J; }
+  p.aS = a.R * a.I * a.J;
+  // B logical (Rb, J, K, Sb)
+  if (!b.trans) { p.bJ = b.R; p.bK = b.R * b.I; }
+  else { p.bK = b.R; p.bJ = b.R * b.J; }
+  p.bS = b.R * b.I * b.J;
+  p.total = p.Ra * p.Rb * p.I * p.K * p.Sa * p.Sb;
+  if (p.total == 0) return;
+  core_product_kernel<<<grid_for(p.total), 256, 0, st>>>(p);
+  CK_LAUNCH();
+  note_launch();
+}
+
+}  // namespace mpob
+
+namespace mpob {
+namespace {
+__global__ void core0_finish_kernel(const double* in, int64_t I1, int64_t K, int64_t R2,
+                                    int64_t kt, const double* sign, double* out) {
+  const int64_t total = I1 * kt * R2;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = idx % I1, l = (idx / I1) % kt, r = idx / (I1 * kt);
+    out[idx] = in[i + I1 * (l + K * r)] * sign[l];
+  }
+}
+__global__ void axpy_kernel(int64_t n, double alpha, const double* x, double* y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] += alpha * x[i];
+}
+__global__ void place_kernel(const double* in, int64_t Ri, int64_t M, int64_t Si, double* out,
+                             int64_t Ro, int64_t So, int64_t ra, int64_t sb) {
+  const int64_t total = Ri * M * Si;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = idx % Ri, m = (idx / Ri) % M, b = idx / (Ri * M);
+    out[(a + ra) + Ro * (m + M * (b + sb))] = in[idx];
+  }
+}
+}  // namespace
+
+void dgemm_axpy(cudaStream_t st, int64_t n, double alpha, const double* x, double* y) {
+  if (n <= 0) return;
+  axpy_kernel<<<grid_for(n), 256, 0, st>>>(n, alpha, x, y);
+  CK_LAUNCH();
+  note_launch();
+}
+
+void place_block(cudaStream_t st, const double* in, int64_t Ri, int64_t M, int64_t Si, double* out,
+                 int64_t Ro, int64_t So, int64_t ra, int64_t sb) {
+  const int64_t total = Ri * M * Si;
+  if (total <= 0) return;
+  (void)So;
+  place_kernel<<<grid_for(total), 256, 0, st>>>(in, Ri, M, Si, out, Ro, So, ra, sb);
+  CK_LAUNCH();
+  note_launch();
+}
+
+void core0_finish(cudaStream_t st, const double* in, int64_t I1, int64_t K, int64_t R2,
+                  int64_t kt, const double* sign_dev, double* out) {
+  const int64_t total = I1 * kt * R2;
+  if (total <= 0) return;
+  core0_finish_kernel<<<grid_for(total), 256, 0, st>>>(in, I1, K, R2, kt, sign_dev, out);
+  CK_LAUNCH();
+  note_launch();
+}
+}  // namespace mpob

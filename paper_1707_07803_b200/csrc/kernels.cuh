@@ -1,0 +1,72 @@
+// Host-side launchers of the sm_100a kernels (all stream-ordered, FP64,
+// column-major).  Each launcher documents the reference operation it
+// replaces.
+#pragma once
+
+#include "common.cuh"
+
+namespace mpob {
+
+__host__ __device__ inline int64_t cdiv_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- dense building blocks (gemm.cu, core_ops.cu) -------------------------
+void dgemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
+           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+           int64_t ldc, int64_t batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0);
+void scale_matrix(cudaStream_t st, int64_t m, int64_t n, double alpha, double* C, int64_t ldc,
+                  int64_t batch = 1, int64_t sC = 0);
+void copy_matrix(cudaStream_t st, int64_t m, int64_t n, const double* A, int64_t lda, double* B,
+                 int64_t ldb);
+void set_identity(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda);
+void fill_zero(cudaStream_t st, double* p, int64_t n);
+// out = in.transpose(perm) for F-ordered arrays of rank <= 6.
+void permute(cudaStream_t st, const double* in, double* out, int rank, const int64_t* dims,
+             const int* perm);
+// Frobenius norm (deterministic two-level reduction) -> device scalar.
+void frob_norm(cudaStream_t st, const double* x, int64_t n, double* out_dev);
+
+// Per-core MPO product (rsvd.py:62-79):
+//   N[a + Ra*c, i, k, b + Sa*d] = sum_j A[a,i,j,b] * B[c,j,k,d]
+// Operands may be logically transposed (swap of axes 1 and 2,
+// mpo.py:402-410) without a copy.
+struct CoreView {
+  const double* p;
+  int64_t R, I, J, S;  // logical extents
+  bool trans;          // physical storage is (R, J, I, S)
+};
+void core_product(cudaStream_t st, const CoreView& a, const CoreView& b, double* out);
+
+// Householder QR of a column-major m x n matrix (qr.cu): on return A holds
+// R in its upper triangle (k = min(m, n) rows) and Q (m x k) is written
+// explicitly; replaces np.linalg.qr(mode="reduced") (LAPACK dgeqrf+dorgqr).
+void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda, double* Q,
+                    int64_t ldq, double* R, int64_t ldr);
+
+// Thin SVD of a column-major m x n matrix (svd.cu).  Returns all min(m,n)
+// singular values (descending, on the device) and the column-sorted
+// factors:  M = Ucarry * Vh  where Ucarry = U * diag(s) (m x k) and
+// Vh (k x n) has orthonormal rows.  Replaces np.linalg.svd(full_matrices=
+// False) (LAPACK dgesdd) at rsvd.py:128 and :189.
+struct SvdOut {
+  DBuf<double> s;       // k
+  DBuf<double> ucarry;  // m x k, column-major, ld = m  (U * diag(s))
+  DBuf<double> vh;      // k x n, column-major, ld = k
+  int64_t k = 0;
+};
+void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ldm, SvdOut& out);
+
+}  // namespace mpob
+
+namespace mpob {
+// W = Ucarry diag(1/s), completed to orthonormal where s == 0 (k x k).
+void svd_left_vectors(cudaStream_t st, int64_t k, const double* ucarry, int64_t ldu,
+                      const double* s, double* W);
+// y += alpha * x (n elements)
+void dgemm_axpy(cudaStream_t st, int64_t n, double alpha, const double* x, double* y);
+// out[(a + ra) + Ro*(m + M*(b + sb))] = in[a + Ri*(m + M*b)]  (mpo_add stacking)
+void place_block(cudaStream_t st, const double* in, int64_t Ri, int64_t M, int64_t Si, double* out,
+                 int64_t Ro, int64_t So, int64_t ra, int64_t sb);
+// out[i, l, r] = in[i, l, r] * sign[l] for l < kt (tnrsvd finishing, rsvd.py:251-257)
+void core0_finish(cudaStream_t st, const double* in, int64_t I1, int64_t K, int64_t R2,
+                  int64_t kt, const double* sign_dev, double* out);
+}  // namespace mpob

@@ -1,0 +1,290 @@
+// Blocked Householder QR on sm_100a, replacing LAPACK dgeqrf + dorgqr behind
+// np.linalg.qr(mode="reduced") at rsvd.py:106 (left-to-right sweep),
+// rsvd.py:132 (exact RQ sweep) and rsvd.py:160 (first-core QR).
+//
+// Panel factorisation: one cooperative kernel per nb-column panel.  The
+// panel's rows are split over up to 148 co-resident CTAs, each keeping its
+// row chunk in shared memory; every column needs two grid-wide reductions
+// (norm, then v^T A_panel), done as per-CTA partials summed in a fixed order
+// (deterministic, no atomics).  The kernel also forms the compact-WY factor
+// T (LAPACK dlarft) from V^T V.  Trailing updates and the explicit Q
+// (dorgqr) are DMMA GEMMs (gemm.cu).  Householder convention as dlarfg:
+// beta = -sign(alpha) * ||x||, tau = (beta - alpha) / beta.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mpob {
+
+namespace {
+
+constexpr int QR_NB = 32;
+constexpr int QR_THREADS = 256;
+
+struct PanelArgs {
+  double* A;       // panel top-left (row j0, col j0)
+  int64_t lda;
+  int64_t mp;      // panel height (m - j0)
+  int w;           // panel width
+  int rpc;         // rows per CTA
+  double* V;       // mp x w explicit reflectors (unit diagonal, zeros above)
+  double* T;       // w x w compact-WY factor (column-major)
+  double* tau;     // w
+  double* part;    // G partial norms
+  double* wpart;   // G x w partial v^T A
+  double* vtv;     // G x w x w partial V^T V
+  double* alpha;   // 1 slot (diagonal element of the current column)
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(PanelArgs p) {
+  extern __shared__ double chunk[];  // rpc x w, column-major: chunk[r + col*ld]
+  __shared__ double red[QR_THREADS / 32];
+  __shared__ double s_scal, s_tau, s_beta;
+  __shared__ double s_w[QR_NB];
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x, c = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int w = p.w;
+  const int64_t r0 = (int64_t)c * p.rpc;
+  const int64_t rem = p.mp - r0;
+  const int nr = rem <= 0 ? 0 : (int)(rem < p.rpc ? rem : p.rpc);
+
+  const int ld = p.rpc;
+  for (int idx = t; idx < nr * w; idx += QR_THREADS) {
+    int r = idx % nr, col = idx / nr;
+    chunk[r + col * ld] = p.A[(r0 + r) + col * p.lda];
+  }
+  __syncthreads();
+
+  for (int jj = 0; jj < w; ++jj) {
+    // phase 1: partial ||x||^2 strictly below the diagonal
+    double s = 0.0;
+    for (int r = t; r < nr; r += QR_THREADS) {
+      int64_t gr = r0 + r;
+      if (gr > jj) { double x = chunk[r + jj * ld]; s = fma(x, x, s); }
+      if (gr == jj) *p.alpha = chunk[r + jj * ld];
+    }
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (t == 0) {
+      double tot = 0.0;
+      for (int i = 0; i < QR_THREADS / 32; ++i) tot += red[i];
+      p.part[c] = tot;
+    }
+    __threadfence();
+    grid.sync();
+    // phase 2: reflector (every CTA computes the same scalars)
+    if (t == 0) {
+      double sig = 0.0;
+      for (int i = 0; i < G; ++i) sig += p.part[i];
+      double al = *p.alpha;
+      double tau = 0.0, beta = al, scal = 0.0;
+      if (sig != 0.0) {
+        double nrm = sqrt(fma(al, al, sig));
+        beta = al >= 0.0 ? -nrm : nrm;
+        tau = (beta - al) / beta;
+        scal = 1.0 / (al - beta);
+      }
+      s_tau = tau; s_beta = beta; s_scal = scal;
+      if (c == 0) p.tau[jj] = tau;
+    }
+    __syncthreads();
+    const double tau = s_tau, scal = s_scal;
+    for (int r = t; r < nr; r += QR_THREADS) {
+      int64_t gr = r0 + r;
+      if (gr > jj) chunk[r + jj * ld] *= scal;
+    }
+    __syncthreads();
+    // partial w_t = sum_r v_r A[r, jj+1+t] over r >= jj (v_jj = 1)
+    const int ncols = w - jj - 1;
+    for (int col = warp; col < ncols; col += QR_THREADS / 32) {
+      double acc = 0.0;
+      for (int r = lane; r < nr; r += 32) {
+        int64_t gr = r0 + r;
+        if (gr >= jj) {
+          double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
+          acc = fma(v, chunk[r + (jj + 1 + col) * ld], acc);
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) p.wpart[(int64_t)c * w + col] = acc;
+    }
+    __threadfence();
+    grid.sync();
+    if (ncols > 0) {
+      for (int col = t; col < ncols; col += QR_THREADS) {
+        double tot = 0.0;
+        for (int i = 0; i < G; ++i) tot += p.wpart[(int64_t)i * w + col];
+        s_w[col] = tot * tau;
+      }
+      __syncthreads();
+      for (int idx = t; idx < nr * ncols; idx += QR_THREADS) {
+        int r = idx % nr, col = idx / nr;
+        int64_t gr = r0 + r;
+        if (gr >= jj) {
+          double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
+          chunk[r + (jj + 1 + col) * ld] -= v * s_w[col];
+        }
+      }
+    }
+    // diagonal of R
+    for (int r = t; r < nr; r += QR_THREADS)
+      if (r0 + r == jj) chunk[r + jj * ld] = s_beta;
+    __syncthreads();
+  }
+
+  // write back R / V parts; explicit V with unit diagonal; partial V^T V
+  for (int idx = t; idx < nr * w; idx += QR_THREADS) {
+    int r = idx % nr, col = idx / nr;
+    int64_t gr = r0 + r;
+    double x = chunk[r + col * ld];
+    p.A[gr + col * p.lda] = x;
+    double v = gr > col ? x : (gr == col ? 1.0 : 0.0);
+    p.V[gr + (int64_t)col * p.mp] = v;
+    chunk[r + col * ld] = v;
+  }
+  __syncthreads();
+  for (int idx = t; idx < w * w; idx += QR_THREADS) {
+    int a = idx % w, b = idx / w;
+    double acc = 0.0;
+    if (a < b)
+      for (int r = 0; r < nr; ++r) acc = fma(chunk[r + a * ld], chunk[r + b * ld], acc);
+    p.vtv[(int64_t)c * w * w + idx] = acc;
+  }
+  __threadfence();
+  grid.sync();
+  if (c == 0) {
+    // dlarft (forward, columnwise): T(0:j, j) = -tau_j T(0:j,0:j) V(:,0:j)^T v_j
+    double* T = p.T;
+    __shared__ double sv[QR_NB * QR_NB];
+    for (int idx = t; idx < w * w; idx += QR_THREADS) {
+      double tot = 0.0;
+      for (int i = 0; i < G; ++i) tot += p.vtv[(int64_t)i * w * w + idx];
+      sv[idx] = tot;  // sv[a + b*w] = v_a . v_b (a < b)
+    }
+    __syncthreads();
+    if (t == 0) {
+      for (int j = 0; j < w; ++j) {
+        double tj = p.tau[j];
+        for (int i = 0; i < j; ++i) {
+          double acc = 0.0;
+          for (int l = i; l < j; ++l) acc += T[i + l * w] * sv[l + j * w];
+          T[i + j * w] = -tj * acc;
+        }
+        T[j + j * w] = tj;
+        for (int i = j + 1; i < w; ++i) T[i + j * w] = 0.0;
+      }
+    }
+  }
+}
+
+__global__ void extract_r_kernel(int64_t k, int64_t n, const double* A, int64_t lda, double* R,
+                                 int64_t ldr) {
+  const int64_t total = k * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = idx % k, j = idx / k;
+    R[i + j * ldr] = (i <= j) ? A[i + j * lda] : 0.0;
+  }
+}
+
+int panel_smem_limit() {
+  static int lim = 0;
+  if (!lim) {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    CK(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            lim - 4096));
+    lim -= 4096;
+  }
+  return lim;
+}
+
+int max_coresident_panel_ctas(size_t smem) {
+  int dev, nsm, per;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qr_panel_kernel, QR_THREADS, smem));
+  return std::max(1, per) * nsm;
+}
+
+}  // namespace
+
+void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda, double* Q,
+                    int64_t ldq, double* R, int64_t ldr) {
+  const int64_t k = std::min(m, n);
+  if (k <= 0) return;
+  const int smax = panel_smem_limit();
+  const int64_t nblk = cdiv(k, QR_NB);
+  DBuf<double> V((size_t)m * k, st);          // panel b's reflectors at column offset j0, ld = mp
+  DBuf<double> T((size_t)nblk * QR_NB * QR_NB, st);
+  DBuf<double> tau(k + QR_NB, st);
+  const int gmax = 148;
+  DBuf<double> part(gmax, st), wpart((size_t)gmax * QR_NB, st),
+      vtv((size_t)gmax * QR_NB * QR_NB, st), alpha(1, st);
+  DBuf<double> W, W2;
+  std::vector<int64_t> voff(nblk);
+  int64_t off = 0;
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t j0 = b * QR_NB;
+    const int w = (int)std::min<int64_t>(QR_NB, k - j0);
+    const int64_t mp = m - j0;
+    voff[b] = off;
+    // rows per CTA: fill up to 148 CTAs, shared memory bound
+    int64_t rpc = std::max<int64_t>(32, cdiv(mp, gmax));
+    size_t smem = (size_t)rpc * w * sizeof(double);
+    if ((int64_t)smem > smax) throw ValueError("QR panel too tall for the cooperative panel kernel");
+    int G = (int)cdiv(mp, rpc);
+    if (G > max_coresident_panel_ctas(smem)) throw CudaError("QR panel grid not co-resident");
+    PanelArgs pa{A + j0 + j0 * lda, lda, mp, w, (int)rpc, V.get() + off,
+                 T.get() + b * QR_NB * QR_NB, tau.get() + j0, part.get(), wpart.get(), vtv.get(),
+                 alpha.get()};
+    void* args[] = {&pa};
+    CK(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QR_THREADS), args, smem,
+                                   st));
+    note_launch();
+    off += mp * w;
+    // trailing update of columns j0+w .. n-1:  A -= V T^T (V^T A)
+    const int64_t nt = n - (j0 + w);
+    if (nt > 0) {
+      double* At = A + j0 + (j0 + w) * lda;
+      if ((int64_t)W.size() < w * nt) { W.alloc((size_t)w * nt, st); W2.alloc((size_t)w * nt, st); }
+      dgemm(st, true, false, w, nt, mp, 1.0, V.get() + voff[b], mp, At, lda, 0.0, W.get(), w);
+      dgemm(st, true, false, w, nt, w, 1.0, T.get() + b * QR_NB * QR_NB, w, W.get(), w, 0.0,
+            W2.get(), w);
+      dgemm(st, false, false, mp, nt, w, -1.0, V.get() + voff[b], mp, W2.get(), w, 1.0, At, lda);
+    }
+  }
+  if (R) {
+    extract_r_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k * n, 256), 2368)), 256,
+                       0, st>>>(k, n, A, lda, R, ldr);
+    CK_LAUNCH();
+    note_launch();
+  }
+  if (!Q) return;
+  // dorgqr: Q = H_1 ... H_k [I; 0], blocks applied last to first
+  set_identity(st, m, k, Q, ldq);
+  for (int64_t b = nblk - 1; b >= 0; --b) {
+    const int64_t j0 = b * QR_NB;
+    const int w = (int)std::min<int64_t>(QR_NB, k - j0);
+    const int64_t mp = m - j0, nq = k - j0;
+    double* Qb = Q + j0 + j0 * ldq;
+    if ((int64_t)W.size() < w * nq) { W.alloc((size_t)w * nq, st); W2.alloc((size_t)w * nq, st); }
+    dgemm(st, true, false, w, nq, mp, 1.0, V.get() + voff[b], mp, Qb, ldq, 0.0, W.get(), w);
+    dgemm(st, false, false, w, nq, w, 1.0, T.get() + b * QR_NB * QR_NB, w, W.get(), w, 0.0,
+          W2.get(), w);
+    dgemm(st, false, false, mp, nq, w, -1.0, V.get() + voff[b], mp, W2.get(), w, 1.0, Qb, ldq);
+  }
+}
+
+}  // namespace mpob

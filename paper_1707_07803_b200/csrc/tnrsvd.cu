@@ -1,0 +1,344 @@
+// TNrSVD pipeline (Algorithms 2-5 of arXiv 1707.07803, as the reference
+// implements them in /root/reference/pkg/src/mposvd/rsvd.py).  The host side
+// here only sequences the sweeps and takes the integer rank decisions
+// (_truncation_rank, mpo.py:297-304) from the device-computed singular
+// values; all arithmetic runs in the sm_100a kernels.
+#include <cmath>
+#include <string>
+
+#include "kernels.cuh"
+#include "tnrsvd.cuh"
+
+namespace mpob {
+
+Core make_core(cudaStream_t st, int64_t R, int64_t I, int64_t J, int64_t S) {
+  Core c;
+  c.R = R; c.I = I; c.J = J; c.S = S;
+  c.buf.alloc((size_t)(R * I * J * S), st);
+  return c;
+}
+
+Cores clone(cudaStream_t st, const Cores& src) {
+  Cores out;
+  out.reserve(src.size());
+  for (const Core& c : src) {
+    Core n = make_core(st, c.R, c.I, c.J, c.S);
+    if (c.size())
+      CK(cudaMemcpyAsync(n.p(), c.p(), sizeof(double) * c.size(), cudaMemcpyDeviceToDevice, st));
+    out.push_back(std::move(n));
+  }
+  return out;
+}
+
+void validate_chain(const Cores& c) {
+  if (c.empty()) throw ValueError("an MPO needs at least one core");
+  for (size_t k = 0; k < c.size(); ++k)
+    if (c[k].R < 1 || c[k].I < 1 || c[k].J < 1 || c[k].S < 1)
+      throw ValueError("core " + std::to_string(k) + " has empty extent");
+  if (c.front().R != 1 || c.back().S != 1) throw ValueError("boundary ranks must be 1");
+  for (size_t k = 0; k + 1 < c.size(); ++k)
+    if (c[k].S != c[k + 1].R)
+      throw ValueError("rank mismatch between cores " + std::to_string(k) + " and " +
+                       std::to_string(k + 1) + ": " + std::to_string(c[k].S) + " vs " +
+                       std::to_string(c[k + 1].R));
+}
+
+// ---- rsvd.py:62-79 ----------------------------------------------------------
+Cores matmul(cudaStream_t st, const Cores& a, bool ta, const Cores& b, bool tb) {
+  if (a.size() != b.size()) throw ValueError("operands must have the same number of cores");
+  for (size_t k = 0; k < a.size(); ++k) {
+    int64_t aj = ta ? a[k].I : a[k].J, bi = tb ? b[k].J : b[k].I;
+    if (aj != bi) throw ValueError("inner dims differ per core");
+  }
+  Cores out;
+  for (size_t k = 0; k < a.size(); ++k) {
+    const Core& x = a[k];
+    const Core& y = b[k];
+    CoreView va{x.p(), x.R, ta ? x.J : x.I, ta ? x.I : x.J, x.S, ta};
+    CoreView vb{y.p(), y.R, tb ? y.J : y.I, tb ? y.I : y.J, y.S, tb};
+    Core n = make_core(st, va.R * vb.R, va.I, vb.J, va.S * vb.S);
+    core_product(st, va, vb, n.p());
+    out.push_back(std::move(n));
+  }
+  return out;
+}
+
+// ---- mpo.py:402-410 ---------------------------------------------------------
+Cores transpose(cudaStream_t st, const Cores& a) {
+  Cores out;
+  for (const Core& c : a) {
+    Core n = make_core(st, c.R, c.J, c.I, c.S);
+    int64_t dims[4] = {c.R, c.I, c.J, c.S};
+    int perm[4] = {0, 2, 1, 3};
+    permute(st, c.p(), n.p(), 4, dims, perm);
+    out.push_back(std::move(n));
+  }
+  return out;
+}
+
+// ---- rsvd.py:82-99 ----------------------------------------------------------
+Cores merge_leading(cudaStream_t st, const Cores& m, int count) {
+  if (count < 1 || count > (int)m.size())
+    throw ValueError("count " + std::to_string(count) + " out of range [1, " +
+                     std::to_string(m.size()) + "]");
+  if (count == 1) return clone(st, m);
+  const Core& c0 = m[0];
+  int64_t A = c0.I, B = c0.J, R = c0.S;
+  DBuf<double> T((size_t)c0.size(), st);
+  CK(cudaMemcpyAsync(T.get(), c0.p(), sizeof(double) * c0.size(), cudaMemcpyDeviceToDevice, st));
+  for (int k = 1; k < count; ++k) {
+    const Core& c = m[k];
+    const int64_t I = c.I, J = c.J, S = c.S;
+    DBuf<double> N((size_t)(A * B * I * J * S), st);
+    dgemm(st, false, false, A * B, I * J * S, R, 1.0, T.get(), A * B, c.p(), R, 0.0, N.get(), A * B);
+    DBuf<double> P((size_t)(A * B * I * J * S), st);
+    int64_t dims[5] = {A, B, I, J, S};
+    int perm[5] = {0, 2, 1, 3, 4};
+    permute(st, N.get(), P.get(), 5, dims, perm);
+    T = std::move(P);
+    A *= I;
+    B *= J;
+    R = S;
+  }
+  Cores out;
+  Core h;
+  h.R = 1; h.I = A; h.J = B; h.S = R;
+  h.buf = std::move(T);
+  out.push_back(std::move(h));
+  for (size_t k = count; k < m.size(); ++k) {
+    Core n = make_core(st, m[k].R, m[k].I, m[k].J, m[k].S);
+    CK(cudaMemcpyAsync(n.p(), m[k].p(), sizeof(double) * m[k].size(), cudaMemcpyDeviceToDevice, st));
+    out.push_back(std::move(n));
+  }
+  return out;
+}
+
+namespace {
+
+// mpo.py:297-304, evaluated on the host from the device singular values
+int64_t truncation_rank(const std::vector<double>& s, double delta, double rel_tol) {
+  const int64_t n = (int64_t)s.size();
+  if (rel_tol == 0.0) {
+    int64_t nz = 0;
+    for (double v : s) nz += (v != 0.0);
+    return std::max<int64_t>(nz, 1);
+  }
+  std::vector<double> tail(n + 1, 0.0);
+  double acc = 0.0;
+  for (int64_t i = n - 1; i >= 0; --i) { acc += s[i] * s[i]; tail[i] = acc; }
+  const double d2 = delta * delta;
+  for (int64_t r = 0; r <= n; ++r)
+    if (tail[r] <= d2) return std::max<int64_t>(r, 1);
+  return std::max<int64_t>(n, 1);
+}
+
+double device_norm(cudaStream_t st, const Core& c) {
+  DBuf<double> nd(1, st);
+  frob_norm(st, c.p(), c.size(), nd.get());
+  double h = 0.0;
+  CK(cudaMemcpyAsync(&h, nd.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return h;
+}
+
+// rsvd.py:102-108
+void l2r(cudaStream_t st, Cores& cores) {
+  for (size_t k = 0; k + 1 < cores.size(); ++k) {
+    Core& c = cores[k];
+    const int64_t m = c.R * c.I * c.J, n = c.S, kk = std::min(m, n);
+    Core q = make_core(st, c.R, c.I, c.J, kk);
+    DBuf<double> rm((size_t)(kk * n), st);
+    householder_qr(st, m, n, c.p(), m, q.p(), m, rm.get(), kk);
+    Core& nx = cores[k + 1];
+    Core nn = make_core(st, kk, nx.I, nx.J, nx.S);
+    dgemm(st, false, false, kk, nx.I * nx.J * nx.S, n, 1.0, rm.get(), kk, nx.p(), n, 0.0, nn.p(), kk);
+    cores[k] = std::move(q);
+    cores[k + 1] = std::move(nn);
+  }
+}
+
+// rsvd.py:111-136
+void r2l(cudaStream_t st, Cores& cores, bool has_tol, double tol) {
+  const size_t d = cores.size();
+  if (d == 1) return;
+  double delta = 0.0;
+  if (has_tol) {
+    l2r(st, cores);
+    delta = tol * device_norm(st, cores.back()) / std::sqrt((double)(d - 1));
+  }
+  for (size_t k = d - 1; k >= 1; --k) {
+    Core& c = cores[k];
+    const int64_t R = c.R, N = c.I * c.J * c.S;
+    Core& pv = cores[k - 1];
+    const int64_t Mp = pv.R * pv.I * pv.J;
+    if (has_tol) {
+      SvdOut o;
+      svd_thin(st, R, N, c.p(), R, o);
+      std::vector<double> s(o.k);
+      CK(cudaMemcpyAsync(s.data(), o.s.get(), sizeof(double) * o.k, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      const int64_t rr = truncation_rank(s, delta, tol);
+      Core nc = make_core(st, rr, c.I, c.J, c.S);
+      copy_matrix(st, rr, N, o.vh.get(), o.k, nc.p(), rr);
+      Core np_ = make_core(st, pv.R, pv.I, pv.J, rr);
+      dgemm(st, false, false, Mp, rr, R, 1.0, pv.p(), Mp, o.ucarry.get(), R, 0.0, np_.p(), Mp);
+      cores[k] = std::move(nc);
+      cores[k - 1] = std::move(np_);
+    } else {
+      const int64_t kk = std::min(N, R);
+      DBuf<double> At((size_t)(N * R), st), Qt((size_t)(N * kk), st), Rt((size_t)(kk * R), st);
+      int64_t dims[2] = {R, N};
+      int perm[2] = {1, 0};
+      permute(st, c.p(), At.get(), 2, dims, perm);
+      householder_qr(st, N, R, At.get(), N, Qt.get(), N, Rt.get(), kk);
+      Core nc = make_core(st, kk, c.I, c.J, c.S);
+      int64_t d2[2] = {N, kk};
+      permute(st, Qt.get(), nc.p(), 2, d2, perm);
+      Core np_ = make_core(st, pv.R, pv.I, pv.J, kk);
+      dgemm(st, false, true, Mp, kk, R, 1.0, pv.p(), Mp, Rt.get(), kk, 0.0, np_.p(), Mp);
+      cores[k] = std::move(nc);
+      cores[k - 1] = std::move(np_);
+    }
+  }
+}
+
+}  // namespace
+
+// ---- mpo.py:323-354 mpo_round: the same L2R QR + R2L truncated-SVD sweep ----
+Cores round_cores(cudaStream_t st, const Cores& m, double rel_tol) {
+  if (rel_tol < 0) throw ValueError("rel_tol must be >= 0");
+  Cores cores = clone(st, m);
+  r2l(st, cores, true, rel_tol);
+  return cores;
+}
+
+// ---- mpo.py:264-294 mpo_add: block-diagonal stacking ----------------------
+Cores add(cudaStream_t st, const Cores& a, const Cores& b) {
+  if (a.size() != b.size())
+    throw ValueError("core counts differ: " + std::to_string(a.size()) + " vs " +
+                     std::to_string(b.size()));
+  for (size_t k = 0; k < a.size(); ++k)
+    if (a[k].I != b[k].I || a[k].J != b[k].J) throw ValueError("per-core row/col extents differ");
+  const size_t d = a.size();
+  Cores out;
+  for (size_t k = 0; k < d; ++k) {
+    const Core& x = a[k];
+    const Core& y = b[k];
+    if (d == 1) {
+      Core n = make_core(st, 1, x.I, x.J, 1);
+      CK(cudaMemcpyAsync(n.p(), x.p(), sizeof(double) * x.size(), cudaMemcpyDeviceToDevice, st));
+      dgemm_axpy(st, x.size(), 1.0, y.p(), n.p());
+      out.push_back(std::move(n));
+      continue;
+    }
+    const int64_t R = (k == 0) ? 1 : x.R + y.R, S = (k == d - 1) ? 1 : x.S + y.S;
+    Core n = make_core(st, R, x.I, x.J, S);
+    fill_zero(st, n.p(), n.size());
+    const int64_t ra = (k == 0) ? 0 : x.R, sa = (k == d - 1) ? 0 : x.S;
+    place_block(st, x.p(), x.R, x.I * x.J, x.S, n.p(), R, S, 0, 0);
+    place_block(st, y.p(), y.R, y.I * y.J, y.S, n.p(), R, S, ra, sa);
+    out.push_back(std::move(n));
+  }
+  return out;
+}
+
+// ---- rsvd.py:139-166 --------------------------------------------------------
+Cores qr(cudaStream_t st, const Cores& y, bool has_tol, double tol, DBuf<double>* r_out) {
+  const Core& f = y[0];
+  if (f.I < f.J)
+    throw ValueError("first core has I1 = " + std::to_string(f.I) + " < K = " +
+                     std::to_string(f.J) + "; merge leading cores first");
+  Cores cores = clone(st, y);
+  r2l(st, cores, has_tol, tol);
+  Core& c0 = cores[0];
+  const int64_t I1 = c0.I, K = c0.J, R2 = c0.S;
+  DBuf<double> Bt((size_t)(I1 * R2 * K), st), Qt((size_t)(I1 * R2 * K), st), Rt((size_t)(K * K), st);
+  int64_t dims[3] = {I1, K, R2};
+  int perm[3] = {0, 2, 1};
+  permute(st, c0.p(), Bt.get(), 3, dims, perm);
+  householder_qr(st, I1 * R2, K, Bt.get(), I1 * R2, Qt.get(), I1 * R2, Rt.get(), K);
+  int64_t d2[3] = {I1, R2, K};
+  permute(st, Qt.get(), c0.p(), 3, d2, perm);
+  if (r_out) *r_out = std::move(Rt);
+  return cores;
+}
+
+// ---- rsvd.py:169-193 --------------------------------------------------------
+Cores svd(cudaStream_t st, const Cores& b, bool has_tol, double tol, DBuf<double>& w,
+          DBuf<double>& s) {
+  const Core& f = b[0];
+  if (f.J < f.I)
+    throw ValueError("first core has J1 = " + std::to_string(f.J) + " < K = " +
+                     std::to_string(f.I) + "; merge leading cores first");
+  Cores cores = clone(st, b);
+  r2l(st, cores, has_tol, tol);
+  Core& c0 = cores[0];
+  const int64_t K = c0.I, N = c0.J * c0.S;
+  SvdOut o;
+  svd_thin(st, K, N, c0.p(), K, o);
+  w.alloc((size_t)(K * K), st);
+  svd_left_vectors(st, K, o.ucarry.get(), K, o.s.get(), w.get());
+  s = std::move(o.s);
+  CK(cudaMemcpyAsync(c0.p(), o.vh.get(), sizeof(double) * K * N, cudaMemcpyDeviceToDevice, st));
+  return transpose(st, cores);
+}
+
+// ---- rsvd.py:196-214 --------------------------------------------------------
+Cores subspace_iteration(cudaStream_t st, const Cores& a, const Cores& o, int q, bool has_tol,
+                         double tol) {
+  if (q < 0) throw ValueError("q must be >= 0");
+  Cores qm = qr(st, matmul(st, a, false, o, false), has_tol, tol, nullptr);
+  for (int it = 0; it < q; ++it) {
+    qm = qr(st, matmul(st, a, true, qm, false), has_tol, tol, nullptr);
+    qm = qr(st, matmul(st, a, false, qm, false), has_tol, tol, nullptr);
+  }
+  return qm;
+}
+
+// ---- rsvd.py:217-259 (after the merge and sketch generation) ---------------
+void tnrsvd(cudaStream_t st, const Cores& am, const Cores& o, int k_target, int q, bool has_tol,
+            double tol, Cores& u, std::vector<double>& s_out, Cores& v) {
+  if (k_target < 1) throw ValueError("k_target must be >= 1");
+  const int64_t K = o[0].J;
+  if (k_target > K) throw ValueError("k_target exceeds the sketch width");
+  Cores qm = subspace_iteration(st, am, o, q, has_tol, tol);
+  Cores b = matmul(st, qm, true, am, false);
+  DBuf<double> w, s;
+  Cores vt = svd(st, b, has_tol, tol, w, s);
+  // U core 0 = einsum("xikr,kl->xilr", Q1, W): batched over r
+  const Core& q0 = qm[0];
+  const int64_t I1 = q0.I, R2 = q0.S;
+  DBuf<double> uc((size_t)(I1 * K * R2), st);
+  dgemm(st, false, false, I1, K, K, 1.0, q0.p(), I1, w.get(), K, 0.0, uc.get(), I1, R2, I1 * K, 0,
+        I1 * K);
+  std::vector<double> wh((size_t)(K * K)), sh((size_t)K);
+  CK(cudaMemcpyAsync(wh.data(), w.get(), sizeof(double) * K * K, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(sh.data(), s.get(), sizeof(double) * K, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  // sign rule rsvd.py:251-255: first nonzero of each kept W column >= 0
+  std::vector<double> sign((size_t)k_target, 1.0);
+  for (int c = 0; c < k_target; ++c)
+    for (int64_t r = 0; r < K; ++r) {
+      double x = wh[(size_t)(r + c * K)];
+      if (x != 0.0) { if (x < 0.0) sign[c] = -1.0; break; }
+    }
+  DBuf<double> sg((size_t)k_target, st);
+  CK(cudaMemcpyAsync(sg.get(), sign.data(), sizeof(double) * k_target, cudaMemcpyHostToDevice, st));
+  u = clone(st, qm);
+  {
+    Core n = make_core(st, 1, I1, k_target, R2);
+    core0_finish(st, uc.get(), I1, K, R2, k_target, sg.get(), n.p());
+    u[0] = std::move(n);
+  }
+  v = std::move(vt);
+  {
+    const Core& v0 = v[0];  // (1, J1, K, R2')
+    Core n = make_core(st, 1, v0.I, k_target, v0.S);
+    core0_finish(st, v0.p(), v0.I, K, v0.S, k_target, sg.get(), n.p());
+    v[0] = std::move(n);
+  }
+  s_out.assign(sh.begin(), sh.begin() + k_target);
+  CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace mpob
