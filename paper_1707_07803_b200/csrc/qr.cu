@@ -203,9 +203,10 @@ int panel_smem_limit() {
     int dev;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    CK(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            lim - 4096));
-    lim -= 4096;
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, qr_panel_kernel));
+    lim -= (int)fa.sharedSizeBytes + 1024;
+    CK(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
   }
   return lim;
 }

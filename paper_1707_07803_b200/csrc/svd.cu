@@ -111,8 +111,9 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(RoundArgs a) {
   for (int idx = t; idx < P2 * P2; idx += JT) {
     int i = idx / P2, j = idx % P2;
     if (i < j) {
-      double gij = G[i * GLD + j], d = G[i * GLD + i] * G[j * GLD + j];
-      if (d > 0.0 && fabs(gij) > a.tol * sqrt(d)) s_skip = 0;
+      // sqrt before multiplying: G_ii * G_jj underflows for graded columns
+      double gij = G[i * GLD + j], d = sqrt(G[i * GLD + i]) * sqrt(G[j * GLD + j]);
+      if (d > 0.0 && fabs(gij) > a.tol * d) s_skip = 0;
     }
   }
   __syncthreads();
@@ -128,7 +129,8 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(RoundArgs a) {
         if (p > q) { int tmp = p; p = q; q = tmp; }
         double gpp = G[p * GLD + p], gqq = G[q * GLD + q], gpq = G[p * GLD + q];
         double c = 1.0, s = 0.0;
-        if (gpp * gqq > 0.0 && fabs(gpq) > a.tol * sqrt(gpp * gqq)) {
+        const double dd = sqrt(gpp) * sqrt(gqq);
+        if (dd > 0.0 && fabs(gpq) > a.tol * dd) {
           double zeta = (gqq - gpp) / (2.0 * gpq);
           double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           c = 1.0 / sqrt(1.0 + tt * tt);
@@ -178,6 +180,36 @@ __global__ void __launch_bounds__(JT) jacobi_round_kernel(RoundArgs a) {
     if (!any) break;
   }
   if (t == 0) *a.flag = 1;
+
+  // re-orthogonalise J (one Newton-Schulz step J <- J (3I - J^T J) / 2):
+  // hundreds of accumulated plane rotations drift O(n_rot * eps) from
+  // orthogonal, which would otherwise build up in V over the sweeps
+  {
+    double* E = G;  // G is no longer needed
+    __syncthreads();
+    for (int idx = t; idx < P2 * P2; idx += JT) {
+      int i = idx / P2, j = idx % P2;
+      double acc = 0.0;
+      for (int l = 0; l < P2; ++l) acc = fma(J[l * GLD + i], J[l * GLD + j], acc);
+      E[i * GLD + j] = acc - (i == j ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    double nv[P2 * P2 / JT];
+#pragma unroll
+    for (int e = 0; e < P2 * P2 / JT; ++e) {
+      int idx = t + e * JT, i = idx / P2, j = idx % P2;
+      double acc = 0.0;
+      for (int l = 0; l < P2; ++l) acc = fma(J[i * GLD + l], E[l * GLD + j], acc);
+      nv[e] = J[i * GLD + j] - 0.5 * acc;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < P2 * P2 / JT; ++e) {
+      int idx = t + e * JT;
+      J[(idx / P2) * GLD + idx % P2] = nv[e];
+    }
+    __syncthreads();
+  }
 
   // ---- 3. apply J to the X and V column blocks (DMMA) ----
   // B fragments of J stay in registers: bj[ks][nt] = J[4ks + (lane&3)][8nt + (lane>>2)]

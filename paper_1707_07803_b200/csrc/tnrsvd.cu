@@ -3,7 +3,9 @@
 // here only sequences the sweeps and takes the integer rank decisions
 // (_truncation_rank, mpo.py:297-304) from the device-computed singular
 // values; all arithmetic runs in the sm_100a kernels.
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "kernels.cuh"
@@ -115,6 +117,27 @@ Cores merge_leading(cudaStream_t st, const Cores& m, int count) {
 
 namespace {
 
+// MPO_B200_TRACE=1: per-call device timing of the dense factorizations
+// (synchronises around each call; diagnostics only)
+struct Trace {
+  bool on;
+  cudaStream_t st;
+  const char* what;
+  int64_t m, n;
+  std::chrono::steady_clock::time_point t0;
+  Trace(cudaStream_t s, const char* w, int64_t mm, int64_t nn) : st(s), what(w), m(mm), n(nn) {
+    static const bool env = std::getenv("MPO_B200_TRACE") != nullptr;
+    on = env;
+    if (on) { cudaStreamSynchronize(st); t0 = std::chrono::steady_clock::now(); }
+  }
+  ~Trace() {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[mpo_b200] %s %lldx%lld %.3f ms\n", what, (long long)m, (long long)n, ms);
+  }
+};
+
 // mpo.py:297-304, evaluated on the host from the device singular values
 int64_t truncation_rank(const std::vector<double>& s, double delta, double rel_tol) {
   const int64_t n = (int64_t)s.size();
@@ -148,7 +171,10 @@ void l2r(cudaStream_t st, Cores& cores) {
     const int64_t m = c.R * c.I * c.J, n = c.S, kk = std::min(m, n);
     Core q = make_core(st, c.R, c.I, c.J, kk);
     DBuf<double> rm((size_t)(kk * n), st);
-    householder_qr(st, m, n, c.p(), m, q.p(), m, rm.get(), kk);
+    {
+      Trace tr(st, "qr", m, n);
+      householder_qr(st, m, n, c.p(), m, q.p(), m, rm.get(), kk);
+    }
     Core& nx = cores[k + 1];
     Core nn = make_core(st, kk, nx.I, nx.J, nx.S);
     dgemm(st, false, false, kk, nx.I * nx.J * nx.S, n, 1.0, rm.get(), kk, nx.p(), n, 0.0, nn.p(), kk);
@@ -173,7 +199,10 @@ void r2l(cudaStream_t st, Cores& cores, bool has_tol, double tol) {
     const int64_t Mp = pv.R * pv.I * pv.J;
     if (has_tol) {
       SvdOut o;
-      svd_thin(st, R, N, c.p(), R, o);
+      {
+        Trace tr(st, "svd", R, N);
+        svd_thin(st, R, N, c.p(), R, o);
+      }
       std::vector<double> s(o.k);
       CK(cudaMemcpyAsync(s.data(), o.s.get(), sizeof(double) * o.k, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
