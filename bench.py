@@ -1,0 +1,420 @@
+"""Benchmark of the B200 TNrSVD / sparse->MPO hot path (BASELINE.json).
+
+Headline workload (N=1): config 2 of BASELINE.json -- TNrSVD of the
+2^20 x 2^20 random MPO (d=20, n=2, rank 8, cores N(0,1)/sqrt(8)), K=20,
+p=10 (oversample 1.5), q=1, round_tol 1e-9.  A "step" is one full TNrSVD
+(time-to-K-triplets).  ``value`` is the reference algorithm's FP64 work
+(the oracle's LAPACK/BLAS flop ledger, bench_data/ledger.json, SURVEY.md
+8(d)) divided by the device time per step, summed over ranks (each rank
+runs an independent replica: TNrSVD does not shard, "replicas only").
+
+The line also carries the conversion metric of BASELINE.json (sparse->MPO
+nnz/s, config 5's 2^22 power-law matrix sharded by nonzeros over the
+ranks with one NCCL all-gather), the FP64 roofline of the dominant kernel,
+the host-CPU baseline (the oracle restatement, numpy/OpenBLAS on this
+box's cores) and the end-to-end number through the public API.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LEDGER = os.path.join(ROOT, "bench_data", "ledger.json")
+METRIC = "TNrSVD time-to-K-triplets as FP64 TFLOP/s (reference flop ledger / device time)"
+UNIT = "TFLOP/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--workload", default="c2")
+    p.add_argument("--no-conversion", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def ledger_flops(name):
+    return float(json.load(open(LEDGER))[name]["flops"])
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline samples (oracle = test infrastructure, only here and in tests)
+# ---------------------------------------------------------------------------
+
+def cpu_tnrsvd_sample(size=2048):
+    """The shapes that dominate config 2's ledger (the B-stage
+    truncation bonds): one dgesdd of a size x 2*size unfolding and one
+    dgeqrf+dorgqr of a 2*size x size unfolding, through the oracle's numpy
+    calls, rated with the same ledger formulas."""
+    from oracle import mposvd_oracle as orc
+    rng = np.random.default_rng(0)
+    m_svd = rng.standard_normal((size, 2 * size))
+    m_qr = rng.standard_normal((2 * size, size))
+    t0 = time.perf_counter()
+    np.linalg.svd(m_svd, full_matrices=False)
+    np.linalg.qr(m_qr)
+    secs = time.perf_counter() - t0
+    flops = orc._svd_flops(size, 2 * size) + orc._qr_flops(2 * size, size)
+    return flops / secs / 1e12, secs, (f"c2 B-stage bond shapes: dgesdd {size}x{2 * size} + "
+                                      f"dgeqrf/dorgqr {2 * size}x{size} (numpy/OpenBLAS)")
+
+
+def cpu_conversion_sample(log2n=18):
+    from oracle import mposvd_oracle as orc
+    from paper_1707_07803_b200.workloads import powerlaw_coo
+    r, c, v = powerlaw_coo(1 << log2n, seed=55)
+    rf = cf = (2,) * log2n
+    t0 = time.perf_counter()
+    orc.conversion_structure(r, c, v, rf, cf)
+    secs = time.perf_counter() - t0
+    return r.size / secs, secs, f"config-5 recipe at 2^{log2n} ({r.size} nnz), oracle sparse.py:234-250"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:  # pragma: no cover
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx = float(f[2])
+                except ValueError:
+                    continue
+                for nm, val in zip(names, f[5:9]):
+                    if val.lower() == "active":
+                        reasons.add(nm)
+        finally:
+            os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_tnrsvd_sample()
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, secs, sample = cpu_tnrsvd_sample()
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c2 TNrSVD (BASELINE configs[1]); CPU sample of its dominant "
+                               "bond factorizations"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": host_cores(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def fp64_peak_tflops(torch):
+    """cuBLAS DGEMM 8192^3 (torch.matmul float64), best of 5: the FP64
+    denominator MEASURED_PEAKS.json lacks."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    del a, b
+    return 2.0 * n ** 3 / best / 1e12
+
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_1707_07803_b200 as m
+    from paper_1707_07803_b200 import _lib
+    from paper_1707_07803_b200.rsvd import prepare, tnrsvd_prepared
+    from paper_1707_07803_b200.workloads import TNRSVD_ARGS, config_mpo
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    name = args.workload
+    kw = dict(TNRSVD_ARGS[name])
+    flops = ledger_flops(name)
+    a_host = config_mpo(name)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    peak = fp64_peak_tflops(torch)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+
+    am, o, kk = prepare(a_host, kw["k_target"], kw["oversample"], kw["seed"])
+
+    def step():
+        u, s, v = tnrsvd_prepared(am, o, kw["k_target"], kw["q"], kw["round_tol"])
+        return s
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = _lib.launch_count()
+    stream = torch.cuda.current_stream()
+    with Clocks(local_rank) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            flush.zero_()
+            s = step()
+        e1.record(stream)
+        e1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    launches = _lib.launch_count() - l0
+    secs = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    per_step = secs / args.steps
+    value = world * flops / per_step / 1e12
+
+    # end to end through the public API: host Mpo in, host Mpo out
+    barrier()
+    torch.cuda.synchronize()
+    h2d = sum(c.nbytes for c in a_host.cores)
+    d2h = 0
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        flush.zero_()
+        lr = m.tnrsvd(a_host, **kw)
+        d2h = sum(c.nbytes for c in lr.u.cores) + sum(c.nbytes for c in lr.v.cores) + lr.s.nbytes
+    e3.record(stream)
+    e3.synchronize()
+    e2e_secs = max_over_ranks(e2.elapsed_time(e3) / 1e3) / args.steps
+    e2e_value = world * flops / e2e_secs / 1e12
+
+    # roofline of the dominant kernel (CUDA events around every Jacobi round kernel)
+    _lib.call("mpo_b200_profile_enable", 1)
+    step()
+    torch.cuda.synchronize()
+    prof = {}
+    import ctypes as C
+    for idx, kname in enumerate(["jacobi_gram_kernel", "jacobi_eig_kernel", "jacobi_apply_kernel"]):
+        ms, fl, n = C.c_double(), C.c_double(), C.c_ulonglong()
+        _lib.call("mpo_b200_profile_read", idx, C.byref(ms), C.byref(fl), C.byref(n))
+        prof[kname] = (ms.value, fl.value, n.value)
+    _lib.call("mpo_b200_profile_enable", 0)
+    dom = max(prof, key=lambda k: prof[k][0])
+    ms_d, fl_d, n_d = prof[dom]
+    if fl_d <= 0:  # eig does no GEMM-shaped work; quote the DMMA kernel with most time
+        dom = max(("jacobi_gram_kernel", "jacobi_apply_kernel"), key=lambda k: prof[k][0])
+        ms_d, fl_d, n_d = prof[dom]
+    achieved = fl_d / (ms_d / 1e3) / 1e12 if ms_d > 0 else 0.0
+    step_ms = per_step * 1e3
+    roofline = {
+        "bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "frac": achieved / peak if peak else None, "traffic": None,
+        "peak_source": "measured in this run: cuBLAS DGEMM 8192^3 (torch.matmul float64); "
+                       "MEASURED_PEAKS.json has no FP64 figure",
+        "avg_launch_us": 1e3 * ms_d / max(n_d, 1), "launches_per_step": n_d,
+        "share_of_step": (ms_d / step_ms) if step_ms else None,
+        "jacobi_ms_per_step": {k: v[0] for k, v in prof.items()},
+    }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy generators of BASELINE.json configs; no dataset)",
+        "config": {"workload": f"{name}: TNrSVD of random MPO d=20 n=2 rank 8 (N(0,1)/sqrt(8)), "
+                               "K=20 p=10 q=1 round_tol=1e-9" if name == "c2" else name,
+                   "parallelism": f"replicas x{world} (independent instances)",
+                   "ledger_flops_per_step": flops, "l2": "flushed (256 MB write) before each step",
+                   "time_to_k_triplets_s": per_step},
+        "roofline": roofline,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "seconds_per_step": e2e_secs,
+                "api": "paper_1707_07803_b200.tnrsvd(host Mpo) -> host U, s, V"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "s_head": [float(x) for x in s[:3]],
+    }
+
+    if not args.no_conversion:
+        line["conversion"] = bench_conversion(args, torch, dist, rank, world, dev, barrier,
+                                              max_over_ranks)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, secs, sample = cpu_tnrsvd_sample()
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "port",
+                                "sample": sample, "seconds": secs}
+        if "conversion" in line:
+            cv, cs, csample = cpu_conversion_sample()
+            line["conversion"]["cpu_baseline"] = {"value": cv, "unit": "nnz/s", "cores": 1,
+                                                  "kind": "port", "sample": csample,
+                                                  "seconds": cs}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def bench_conversion(args, torch, dist, rank, world, dev, barrier, max_over_ranks):
+    """Config 5's conversion: 2^22 square, power-law rows (alpha 2.1), uniform
+    columns, U(-1,1) values, plan ([2]*22, [2]*22); nnz sharded over ranks."""
+    from paper_1707_07803_b200.distributed import DeviceOps, convert_sharded, shard_range
+    from paper_1707_07803_b200.workloads import powerlaw_coo, square_plan
+    r, c, v = powerlaw_coo(1 << 22, seed=55)
+    n = r.size
+    lo, hi = shard_range(n, world, rank)
+    tr = torch.from_numpy(r[lo:hi]).to(dev)
+    tc = torch.from_numpy(c[lo:hi]).to(dev)
+    tv = torch.from_numpy(v[lo:hi]).to(dev)
+    plan = square_plan(22)
+    ops = DeviceOps(dev.index)
+    for _ in range(args.warmup):
+        res = convert_sharded(tr, tc, tv, plan, ops)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        res = convert_sharded(tr, tc, tv, plan, ops)
+    e1.record()
+    e1.synchronize()
+    secs = max_over_ranks(e0.elapsed_time(e1) / 1e3) / args.steps
+    blocks = res.rank
+    compulsory = 32.0 * n + 8.0 * blocks   # read 24 B/nnz, write ti 8 B, uniq 8 B
+    peak_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6521.1
+    achieved = compulsory / secs / 1e9 / world   # per GPU
+    # end to end: host COO in, host (i1, j1, ti, values, uniq) out
+    import paper_1707_07803_b200 as m
+    rs, cs_, vs = r[lo:hi], c[lo:hi], v[lo:hi]
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        rr = m.convert_structure(rs, cs_, vs, plan)
+        arrs = rr.arrays()
+        rr.free()
+    e2e = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    return {
+        "metric": "sparse->MPO conversion nnz/s (config 5, 2^22 power-law, d=22)",
+        "value": n / secs, "unit": "nnz/s", "n_gpus": world, "scaling": "strong",
+        "nnz": int(n), "blocks": int(blocks), "ms_per_step": secs * 1e3,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
+                     "frac": achieved / peak_hbm,
+                     "traffic": None, "algorithmic_bytes_per_step": compulsory,
+                     "note": "whole conversion (compaction + 6 radix passes + segment) timed; "
+                             "compulsory bytes 32 B/nnz + 8 B/block"},
+        "e2e": {"value": (hi - lo) * world / e2e if world > 1 else n / e2e, "unit": "nnz/s",
+                "h2d_bytes_per_step": int(24 * (hi - lo)),
+                "d2h_bytes_per_step": int(sum(a.nbytes for a in arrs)),
+                "api": "convert_structure(host COO) + arrays() (single-rank shard path)"},
+    }
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

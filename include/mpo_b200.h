@@ -42,6 +42,10 @@ typedef struct mpo_conv mpo_conv; /* conversion structure (sparse.py:207 result)
 const char* mpo_b200_last_error(void);
 int mpo_b200_abi_version(void);
 unsigned long long mpo_b200_launch_count(void); /* kernels launched so far */
+/* CUDA-event timing of the block-Jacobi round kernels (bench roofline):
+ * which = 0 jacobi_gram, 1 jacobi_eig, 2 jacobi_apply; enable(1) resets. */
+int mpo_b200_profile_enable(int on);
+int mpo_b200_profile_read(int which, double* ms, double* flops, unsigned long long* launches);
 
 int mpo_ctx_create(int device, void* cuda_stream, mpo_ctx** out);
 int mpo_ctx_set_stream(mpo_ctx* ctx, void* cuda_stream);

@@ -27,6 +27,8 @@ SIGNATURES = {
     "mpo_b200_last_error": (C.c_char_p, []),
     "mpo_b200_abi_version": (C.c_int, []),
     "mpo_b200_launch_count": (C.c_ulonglong, []),
+    "mpo_b200_profile_enable": (C.c_int, [C.c_int]),
+    "mpo_b200_profile_read": (C.c_int, [C.c_int, _DP, _DP, C.POINTER(C.c_ulonglong)]),
     "mpo_ctx_create": (C.c_int, [C.c_int, _P, C.POINTER(_P)]),
     "mpo_ctx_set_stream": (C.c_int, [_P, _P]),
     "mpo_ctx_synchronize": (C.c_int, [_P]),

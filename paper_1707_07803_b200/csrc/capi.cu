@@ -82,6 +82,21 @@ MPO_API const char* mpo_b200_last_error(void) { return g_err.c_str(); }
 MPO_API int mpo_b200_abi_version(void) { return 1; }
 MPO_API unsigned long long mpo_b200_launch_count(void) { return mpob::g_launches; }
 
+MPO_API int mpo_b200_profile_enable(int on) {
+  mpob::g_prof.on = on != 0;
+  mpob::g_prof.reset();
+  return MPO_OK;
+}
+
+MPO_API int mpo_b200_profile_read(int which, double* ms, double* flops,
+                                  unsigned long long* launches) {
+  if (which < 0 || which > 2) { g_err = "profile index out of range"; return MPO_EVALUE; }
+  *ms = mpob::g_prof.ms[which];
+  *flops = mpob::g_prof.flops[which];
+  *launches = mpob::g_prof.launches[which];
+  return MPO_OK;
+}
+
 MPO_API int mpo_ctx_create(int device, void* stream, mpo_ctx** out) {
   return guarded(nullptr, [&] {
     need(out != nullptr, "null output pointer");

@@ -7,6 +7,18 @@
 
 namespace mpob {
 
+// Optional per-kernel CUDA-event timing of the Jacobi rounds (bench.py's
+// roofline): 0 = jacobi_gram, 1 = jacobi_eig, 2 = jacobi_apply.
+struct KernelProfile {
+  bool on = false;
+  double ms[3] = {0, 0, 0};
+  double flops[3] = {0, 0, 0};
+  unsigned long long launches[3] = {0, 0, 0};
+  void add(int k, double t, double f) { ms[k] += t; flops[k] += f; launches[k] += 1; }
+  void reset() { for (int k = 0; k < 3; ++k) { ms[k] = 0; flops[k] = 0; launches[k] = 0; } }
+};
+extern KernelProfile g_prof;
+
 __host__ __device__ inline int64_t cdiv_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // ---- dense building blocks (gemm.cu, core_ops.cu) -------------------------

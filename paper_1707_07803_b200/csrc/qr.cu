@@ -187,6 +187,156 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(PanelArgs p) {
   }
 }
 
+// Cluster variant of the panel factorisation: the panel's rows are split
+// over the CTAs of ONE thread-block cluster (<= 16 SMs); the two reductions
+// per column go through distributed shared memory and cluster barriers
+// (~0.2 us) instead of global memory and grid-wide barriers.
+struct ClusterPanelArgs {
+  double* A;
+  int64_t lda;
+  int64_t mp;
+  int w;
+  int rpc;
+  double* V;
+  double* T;
+  double* tau;
+};
+
+__global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPanelArgs p) {
+  extern __shared__ double chunk[];  // rpc x w, column-major
+  __shared__ double s_part, s_alpha;
+  __shared__ double s_wpart[QR_NB];
+  __shared__ double s_w[QR_NB];
+  __shared__ double s_vtv[QR_NB * QR_NB];
+  __shared__ double s_tau[QR_NB];
+  __shared__ double red[QR_THREADS / 32];
+  __shared__ double s_scal, s_tauj, s_beta;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CS = (int)cluster.num_blocks(), c = (int)cluster.block_rank();
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int w = p.w, ld = p.rpc;
+  const int64_t r0 = (int64_t)c * p.rpc;
+  const int64_t rem = p.mp - r0;
+  const int nr = rem <= 0 ? 0 : (int)(rem < p.rpc ? rem : p.rpc);
+  for (int idx = t; idx < nr * w; idx += QR_THREADS) {
+    int r = idx % nr, col = idx / nr;
+    chunk[r + col * ld] = p.A[(r0 + r) + col * p.lda];
+  }
+  __syncthreads();
+  for (int jj = 0; jj < w; ++jj) {
+    double s = 0.0;
+    for (int r = t; r < nr; r += QR_THREADS) {
+      int64_t gr = r0 + r;
+      if (gr > jj) { double x = chunk[r + jj * ld]; s = fma(x, x, s); }
+      if (gr == jj) s_alpha = chunk[r + jj * ld];
+    }
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (t == 0) {
+      double tot = 0.0;
+      for (int i = 0; i < QR_THREADS / 32; ++i) tot += red[i];
+      s_part = tot;
+    }
+    cluster.sync();
+    if (t == 0) {
+      double sig = 0.0;
+      for (int i = 0; i < CS; ++i) sig += *cluster.map_shared_rank(&s_part, i);
+      const double al = *cluster.map_shared_rank(&s_alpha, (int)(jj / p.rpc));
+      double tau = 0.0, beta = al, scal = 0.0;
+      if (sig != 0.0) {
+        double nrm = sqrt(fma(al, al, sig));
+        beta = al >= 0.0 ? -nrm : nrm;
+        tau = (beta - al) / beta;
+        scal = 1.0 / (al - beta);
+      }
+      s_tauj = tau; s_beta = beta; s_scal = scal;
+      s_tau[jj] = tau;
+    }
+    __syncthreads();
+    const double scal = s_scal;
+    for (int r = t; r < nr; r += QR_THREADS)
+      if (r0 + r > jj) chunk[r + jj * ld] *= scal;
+    __syncthreads();
+    const int ncols = w - jj - 1;
+    for (int col = warp; col < ncols; col += QR_THREADS / 32) {
+      double acc = 0.0;
+      for (int r = lane; r < nr; r += 32) {
+        int64_t gr = r0 + r;
+        if (gr >= jj) {
+          double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
+          acc = fma(v, chunk[r + (jj + 1 + col) * ld], acc);
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) s_wpart[col] = acc;
+    }
+    cluster.sync();
+    if (ncols > 0) {
+      const double tau = s_tauj;
+      for (int col = t; col < ncols; col += QR_THREADS) {
+        double tot = 0.0;
+        for (int i = 0; i < CS; ++i) tot += cluster.map_shared_rank(s_wpart, i)[col];
+        s_w[col] = tot * tau;
+      }
+      __syncthreads();
+      for (int idx = t; idx < nr * ncols; idx += QR_THREADS) {
+        int r = idx % nr, col = idx / nr;
+        int64_t gr = r0 + r;
+        if (gr >= jj) {
+          double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
+          chunk[r + (jj + 1 + col) * ld] -= v * s_w[col];
+        }
+      }
+    }
+    for (int r = t; r < nr; r += QR_THREADS)
+      if (r0 + r == jj) chunk[r + jj * ld] = s_beta;
+    __syncthreads();
+  }
+  for (int idx = t; idx < nr * w; idx += QR_THREADS) {
+    int r = idx % nr, col = idx / nr;
+    int64_t gr = r0 + r;
+    double x = chunk[r + col * ld];
+    p.A[gr + col * p.lda] = x;
+    double v = gr > col ? x : (gr == col ? 1.0 : 0.0);
+    p.V[gr + (int64_t)col * p.mp] = v;
+    chunk[r + col * ld] = v;
+  }
+  __syncthreads();
+  for (int idx = t; idx < w * w; idx += QR_THREADS) {
+    int a = idx % w, b = idx / w;
+    double acc = 0.0;
+    if (a < b)
+      for (int r = 0; r < nr; ++r) acc = fma(chunk[r + a * ld], chunk[r + b * ld], acc);
+    s_vtv[idx] = acc;
+  }
+  cluster.sync();
+  if (c == 0) {
+    // sum the V^T V partials (fixed rank order) in place, then dlarft
+    for (int idx = t; idx < w * w; idx += QR_THREADS) {
+      double tot = 0.0;
+      for (int i = 0; i < CS; ++i) tot += cluster.map_shared_rank(s_vtv, i)[idx];
+      chunk[idx] = tot;  // reuse own chunk (already written back)
+    }
+    __syncthreads();
+    if (t == 0) {
+      double* T = p.T;
+      for (int j = 0; j < w; ++j) {
+        const double tj = s_tau[j];
+        p.tau[j] = tj;
+        for (int i = 0; i < j; ++i) {
+          double acc = 0.0;
+          for (int l = i; l < j; ++l) acc += T[i + l * w] * chunk[l + j * w];
+          T[i + j * w] = -tj * acc;
+        }
+        T[j + j * w] = tj;
+        for (int i = j + 1; i < w; ++i) T[i + j * w] = 0.0;
+      }
+    }
+  }
+  cluster.sync();  // keep every CTA's shared memory alive until rank 0 is done
+}
+
 __global__ void extract_r_kernel(int64_t k, int64_t n, const double* A, int64_t lda, double* R,
                                  int64_t ldr) {
   const int64_t total = k * n;
@@ -207,6 +357,23 @@ int panel_smem_limit() {
     CK(cudaFuncGetAttributes(&fa, qr_panel_kernel));
     lim -= (int)fa.sharedSizeBytes + 1024;
     CK(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+  }
+  return lim;
+}
+
+int cluster_smem_limit() {
+  static int lim = 0;
+  if (!lim) {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, qr_panel_cluster_kernel));
+    lim -= (int)fa.sharedSizeBytes + 1024;
+    CK(cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            lim));
+    CK(cudaFuncSetAttribute(qr_panel_cluster_kernel,
+                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   }
   return lim;
 }
@@ -242,17 +409,39 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
     const int64_t mp = m - j0;
     voff[b] = off;
     // rows per CTA: fill up to 148 CTAs, shared memory bound
-    int64_t rpc = std::max<int64_t>(32, cdiv(mp, gmax));
-    size_t smem = (size_t)rpc * w * sizeof(double);
-    if ((int64_t)smem > smax) throw ValueError("QR panel too tall for the cooperative panel kernel");
-    int G = (int)cdiv(mp, rpc);
-    if (G > max_coresident_panel_ctas(smem)) throw CudaError("QR panel grid not co-resident");
-    PanelArgs pa{A + j0 + j0 * lda, lda, mp, w, (int)rpc, V.get() + off,
-                 T.get() + b * QR_NB * QR_NB, tau.get() + j0, part.get(), wpart.get(), vtv.get(),
-                 alpha.get()};
-    void* args[] = {&pa};
-    CK(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QR_THREADS), args, smem,
-                                   st));
+    // preferred: one thread-block cluster (<= 16 CTAs, DSMEM reductions)
+    const int64_t crpc = cdiv(std::max<int64_t>(64, cdiv(mp, 16)), 8) * 8;
+    const size_t csmem = (size_t)crpc * w * sizeof(double);
+    if ((int64_t)csmem <= cluster_smem_limit()) {
+      const int CS = (int)cdiv(mp, crpc);
+      ClusterPanelArgs ca{A + j0 + j0 * lda, lda, mp, w, (int)crpc, V.get() + off,
+                          T.get() + b * QR_NB * QR_NB, tau.get() + j0};
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CS);
+      cfg.blockDim = dim3(QR_THREADS);
+      cfg.dynamicSmemBytes = csmem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = CS;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CK(cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel, ca));
+    } else {
+      int64_t rpc = std::max<int64_t>(32, cdiv(mp, gmax));
+      size_t smem = (size_t)rpc * w * sizeof(double);
+      if ((int64_t)smem > smax) throw ValueError("QR panel too tall for the cooperative panel kernel");
+      int G = (int)cdiv(mp, rpc);
+      if (G > max_coresident_panel_ctas(smem)) throw CudaError("QR panel grid not co-resident");
+      PanelArgs pa{A + j0 + j0 * lda, lda, mp, w, (int)rpc, V.get() + off,
+                   T.get() + b * QR_NB * QR_NB, tau.get() + j0, part.get(), wpart.get(), vtv.get(),
+                   alpha.get()};
+      void* args[] = {&pa};
+      CK(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QR_THREADS), args, smem,
+                                     st));
+    }
     note_launch();
     off += mp * w;
     // trailing update of columns j0+w .. n-1:  A -= V T^T (V^T A)

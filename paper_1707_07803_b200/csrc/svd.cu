@@ -4,18 +4,26 @@
 //
 // Algorithm: QR preconditioning (Householder QR of the tall orientation,
 // qr.cu) followed by one-sided block Jacobi (Hestenes) on the k x k
-// triangular factor X.  Columns are grouped in blocks of JB = 16; each
-// round of the round-robin tournament pairs every block with another, and
-// one CTA per pair
-//   1. forms the 32 x 32 Gram matrix of its two column blocks (DMMA),
-//   2. diagonalises it in shared memory with cyclic two-sided Jacobi
-//      (rotations accumulated into J), and
-//   3. applies J to the X and V column blocks (DMMA).
-// A sweep is nb-1 rounds; iteration stops when a whole sweep performs no
-// rotation (every pair has |x_p.x_q| <= tol ||x_p|| ||x_q||), which gives
-// singular values to absolute accuracy O(eps ||M||) like dgesdd.  Singular
-// values are the final column norms, sorted descending with index
-// tie-break (deterministic).  No atomics anywhere.
+// triangular factor X (zero-padded to kp x kp, kp a multiple of 32).
+// Columns are grouped in blocks of JB = 16; a sweep is the nb-1 rounds of a
+// round-robin tournament over the nb blocks.  Each round is three kernels:
+//   gram  : (pair, row split) CTAs stream their rows of the pair's 32
+//           columns through shared memory (cp.async double buffering) and
+//           form a partial 32 x 32 Gram matrix on the DMMA pipe;
+//   eig   : one CTA per pair sums the partials in a fixed order, tests
+//           convergence, diagonalises the Gram matrix with cyclic two-sided
+//           Jacobi in shared memory and re-orthogonalises the accumulated
+//           rotation J (one Newton-Schulz step);
+//   apply : (pair, row split, X|V) CTAs stream rows again and multiply by J
+//           on the DMMA pipe, in place.
+// Iteration stops after a sweep in which no pair needed rotating
+// (|x_p.x_q| <= tol ||x_p|| ||x_q|| for every column pair), which gives
+// singular values to O(eps ||M||) like dgesdd.  Singular values are the
+// final column norms, sorted descending with index tie-break.  No atomics,
+// fixed reduction orders: bitwise deterministic.
+#include <chrono>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -23,12 +31,13 @@ namespace mpob {
 
 namespace {
 
-constexpr int JB = 16;          // columns per Jacobi block
-constexpr int P2 = 2 * JB;      // columns per pair
-constexpr int CH = 64;          // rows per streamed chunk
-constexpr int CLD = P2 + 4;     // chunk row stride (doubles): conflict-free fragments
+constexpr int JB = 16;        // columns per Jacobi block
+constexpr int P2 = 2 * JB;    // columns per pair
+constexpr int CH = 64;        // rows per streamed chunk
+constexpr int LDR = CH + 4;   // chunk column stride (doubles): conflict-free DMMA fragments
 constexpr int GLD = P2 + 1;
 constexpr int JT = 256;
+constexpr int NSEG = P2 * CH / 2;  // 16-byte segments per chunk
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile(
@@ -38,217 +47,271 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void pair_of_round(int nb, int r, int i, int& x, int& y) {
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__host__ __device__ __forceinline__ void pair_of_round(int nb, int r, int i, int& x, int& y) {
   // circle method: slot 0 fixed, slots 1..nb-1 rotate by r
   auto slot = [&](int j) { return j == 0 ? 0 : 1 + ((j - 1 + r) % (nb - 1)); };
   x = slot(i);
   y = slot(nb - 1 - i);
 }
 
-struct RoundArgs {
-  double* X;     // rows x ncols_pad, ld = ldx
-  int64_t ldx, rows;
-  double* V;     // vrows x ncols_pad, ld = ldv
-  int64_t ldv, vrows;
-  int nb, round;
-  double tol;
-  int* flag;     // set to 1 when any rotation happened
-};
-
-// stream the 2*JB columns of blocks (bx, by) through shared memory
 __device__ __forceinline__ int64_t gcol(int c, int bx, int by) {
   return c < JB ? (int64_t)bx * JB + c : (int64_t)by * JB + (c - JB);
 }
 
-__global__ void __launch_bounds__(JT) jacobi_round_kernel(RoundArgs a) {
+// issue the cp.async loads of rows [r0, r0 + CH) of the pair's 32 columns
+__device__ __forceinline__ void load_chunk(double* buf, const double* M, int64_t ld,
+                                           int64_t r0, int64_t rend, int bx, int by) {
+  for (int s = threadIdx.x; s < NSEG; s += JT) {
+    const int c = s / (CH / 2), rp = s % (CH / 2);
+    const int64_t gr = r0 + 2 * rp;
+    const bool ok = gr < rend;  // rows come in pairs (kp is even)
+    const double* src = M + (ok ? gr : 0) + gcol(c, bx, by) * ld;
+    cp_async16(buf + c * LDR + 2 * rp, src, ok ? 16 : 0);
+  }
+}
+
+struct JacArgs {
+  double* X;
+  double* V;
+  int64_t ld;      // = kp (both matrices kp x kp)
+  int64_t rows;    // = kp
+  int nb, round, splits;
+  int64_t rps;     // rows per split (multiple of CH)
+  double* gpart;   // npairs * splits * P2*P2
+  double* J;       // npairs * P2*P2 (row-major)
+  int* skip;       // npairs
+  int* flag;       // any rotation in this sweep
+  double tol;
+  int inner;       // max inner (32 x 32 Gram) Jacobi sweeps per outer round
+  int* skiplog;    // profiling only: per (round, pair) skip flags, or null
+};
+
+__global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
+  __shared__ __align__(16) double buf[2][P2 * LDR];
+  const int pair = blockIdx.x, split = blockIdx.y;
+  int bx, by;
+  pair_of_round(a.nb, a.round, pair, bx, by);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
+  const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  const int nch = (int)cdiv_dev(re - rb, CH);
+  if (nch > 0) load_chunk(buf[0], a.X, a.ld, rb, re, bx, by);
+  cp_async_commit();
+  for (int i = 0; i < nch; ++i) {
+    if (i + 1 < nch) load_chunk(buf[(i + 1) & 1], a.X, a.ld, rb + (int64_t)(i + 1) * CH, re, bx, by);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* b = buf[i & 1];
+    const double* pa = b + (ti * 8 + (lane >> 2)) * LDR + (lane & 3);
+    const double* pb0 = b + (tj0 * 8 + (lane >> 2)) * LDR + (lane & 3);
+    const double* pb1 = pb0 + 8 * LDR;
+#pragma unroll
+    for (int k0 = 0; k0 < CH; k0 += 4) {
+      const double av = pa[k0];
+      dmma(acc[0], av, pb0[k0]);
+      dmma(acc[1], av, pb1[k0]);
+    }
+    __syncthreads();
+  }
+  double* G = a.gpart + ((int64_t)pair * a.splits + split) * (P2 * P2);
+  const int gi = ti * 8 + (lane >> 2);
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) G[gi * P2 + (tj0 + u) * 8 + 2 * (lane & 3) + e] = acc[u][e];
+}
+
+__global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
   __shared__ double G[P2 * GLD];
   __shared__ double J[P2 * GLD];
-  __shared__ double chunk[CH * CLD];
-  __shared__ double rc[P2 / 2], rs[P2 / 2];
-  __shared__ int rp[P2 / 2], rq[P2 / 2];
-  __shared__ int s_any, s_skip;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  int bx, by;
-  pair_of_round(a.nb, a.round, blockIdx.x, bx, by);
-
-  // ---- 1. Gram matrix of the 32 columns (DMMA over row chunks) ----
-  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  for (int64_t r0 = 0; r0 < a.rows; r0 += CH) {
-    __syncthreads();
-    for (int idx = t; idx < CH * P2; idx += JT) {
-      int r = idx % CH, c = idx / CH;
-      int64_t gr = r0 + r;
-      chunk[r * CLD + c] = gr < a.rows ? a.X[gr + gcol(c, bx, by) * a.ldx] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int k0 = 0; k0 < CH; k0 += 4) {
-      const double* row = chunk + (k0 + (lane & 3)) * CLD + (lane >> 2);
-      double av = row[ti * 8];
-      dmma(acc[0], av, row[tj0 * 8]);
-      dmma(acc[1], av, row[(tj0 + 1) * 8]);
-    }
+  __shared__ int s_skip;
+  const int t = threadIdx.x, pair = blockIdx.x;
+  for (int idx = t; idx < P2 * P2; idx += JT) {
+    const double* gp = a.gpart + (int64_t)pair * a.splits * (P2 * P2) + idx;
+    double s = 0.0;
+    for (int sp = 0; sp < a.splits; ++sp) s += gp[(int64_t)sp * P2 * P2];
+    G[(idx / P2) * GLD + idx % P2] = s;
+    J[(idx / P2) * GLD + idx % P2] = (idx / P2 == idx % P2) ? 1.0 : 0.0;
   }
-  {
-    const int gi = ti * 8 + (lane >> 2);
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) G[gi * GLD + (tj0 + u) * 8 + 2 * (lane & 3) + e] = acc[u][e];
-  }
-  for (int idx = t; idx < P2 * P2; idx += JT) J[(idx / P2) * GLD + idx % P2] = (idx / P2 == idx % P2) ? 1.0 : 0.0;
-  if (t == 0) { s_any = 0; s_skip = 1; }
+  if (t == 0) s_skip = 1;
   __syncthreads();
-  // symmetrise (the two halves come from different DMMA tiles; use the
-  // upper one for both so the inner problem is exactly symmetric)
+  // symmetrise from the upper triangle
   for (int idx = t; idx < P2 * P2; idx += JT) {
     int i = idx / P2, j = idx % P2;
     if (i > j) G[i * GLD + j] = G[j * GLD + i];
   }
   __syncthreads();
-  // convergence test over all column pairs of the two blocks
   for (int idx = t; idx < P2 * P2; idx += JT) {
     int i = idx / P2, j = idx % P2;
     if (i < j) {
       // sqrt before multiplying: G_ii * G_jj underflows for graded columns
-      double gij = G[i * GLD + j], d = sqrt(G[i * GLD + i]) * sqrt(G[j * GLD + j]);
-      if (d > 0.0 && fabs(gij) > a.tol * d) s_skip = 0;
+      double d = sqrt(G[i * GLD + i]) * sqrt(G[j * GLD + j]);
+      if (d > 0.0 && fabs(G[i * GLD + j]) > a.tol * d) s_skip = 0;
     }
   }
   __syncthreads();
+  if (t == 0) {
+    a.skip[pair] = s_skip;
+    if (a.skiplog) a.skiplog[(int64_t)a.round * gridDim.x + pair] = s_skip;
+  }
   if (s_skip) return;
+  if (t == 0) *a.flag = 1;
 
-  // ---- 2. cyclic two-sided Jacobi on G (parallel circle ordering) ----
-  for (int sweep = 0; sweep < 12; ++sweep) {
+  // cyclic two-sided Jacobi on G (parallel circle ordering).  Warp w owns
+  // pairs 2w and 2w+1 of every round: it computes their rotations
+  // redundantly in all lanes, then updates the pairs' columns (lane = row)
+  // and, after a CTA barrier, their rows (lane = column); two barriers per
+  // round, no shared rotation tables.
+  const int lane = t & 31, warp = t >> 5;
+  for (int sweep = 0; sweep < a.inner; ++sweep) {
     int any = 0;
     for (int r = 0; r < P2 - 1; ++r) {
-      if (t < P2 / 2) {
+      int pp[2], qq[2];
+      double cc[2], ss[2], dp[2], dq[2];
+      bool rot[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
         int p, q;
-        pair_of_round(P2, r, t, p, q);
+        pair_of_round(P2, r, 2 * warp + u, p, q);
         if (p > q) { int tmp = p; p = q; q = tmp; }
-        double gpp = G[p * GLD + p], gqq = G[q * GLD + q], gpq = G[p * GLD + q];
-        double c = 1.0, s = 0.0;
+        const double gpp = G[p * GLD + p], gqq = G[q * GLD + q], gpq = G[p * GLD + q];
         const double dd = sqrt(gpp) * sqrt(gqq);
-        if (dd > 0.0 && fabs(gpq) > a.tol * dd) {
-          double zeta = (gqq - gpp) / (2.0 * gpq);
-          double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        rot[u] = dd > 0.0 && fabs(gpq) > a.tol * dd;
+        double c = 1.0, s = 0.0, tt = 0.0;
+        if (rot[u]) {
+          const double zeta = (gqq - gpp) / (2.0 * gpq);
+          tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           c = 1.0 / sqrt(1.0 + tt * tt);
           s = tt * c;
         }
-        rp[t] = p; rq[t] = q; rc[t] = c; rs[t] = s;
+        pp[u] = p; qq[u] = q; cc[u] = c; ss[u] = s;
+        dp[u] = gpp - tt * gpq;   // exact-formula diagonal after the rotation
+        dq[u] = gqq + tt * gpq;
+        any |= rot[u];
+      }
+      __syncwarp();
+      // columns p, q of G and J: (col_p, col_q) <- (c col_p - s col_q, s col_p + c col_q)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!rot[u]) continue;
+        const int p = pp[u], q = qq[u];
+        const double c = cc[u], s = ss[u];
+        const double gp = G[lane * GLD + p], gq = G[lane * GLD + q];
+        G[lane * GLD + p] = c * gp - s * gq;
+        G[lane * GLD + q] = s * gp + c * gq;
+        const double jp = J[lane * GLD + p], jq = J[lane * GLD + q];
+        J[lane * GLD + p] = c * jp - s * jq;
+        J[lane * GLD + q] = s * jp + c * jq;
       }
       __syncthreads();
-      // column update of G and J: (col_p, col_q) <- (c col_p - s col_q, s col_p + c col_q)
-      for (int idx = t; idx < (P2 / 2) * P2; idx += JT) {
-        int pr = idx / P2, j = idx % P2;
-        double c = rc[pr], s = rs[pr];
-        if (s != 0.0) {
-          int p = rp[pr], q = rq[pr];
-          double gp = G[j * GLD + p], gq = G[j * GLD + q];
-          G[j * GLD + p] = c * gp - s * gq;
-          G[j * GLD + q] = s * gp + c * gq;
-          double jp = J[j * GLD + p], jq = J[j * GLD + q];
-          J[j * GLD + p] = c * jp - s * jq;
-          J[j * GLD + q] = s * jp + c * jq;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!rot[u]) continue;
+        const int p = pp[u], q = qq[u];
+        const double c = cc[u], s = ss[u];
+        const double gp = G[p * GLD + lane], gq = G[q * GLD + lane];
+        G[p * GLD + lane] = c * gp - s * gq;
+        G[q * GLD + lane] = s * gp + c * gq;
+      }
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!rot[u]) continue;
+          G[pp[u] * GLD + qq[u]] = 0.0;
+          G[qq[u] * GLD + pp[u]] = 0.0;
+          G[pp[u] * GLD + pp[u]] = dp[u];
+          G[qq[u] * GLD + qq[u]] = dq[u];
         }
       }
       __syncthreads();
-      // row update of G
-      for (int idx = t; idx < (P2 / 2) * P2; idx += JT) {
-        int pr = idx / P2, j = idx % P2;
-        double c = rc[pr], s = rs[pr];
-        if (s != 0.0) {
-          int p = rp[pr], q = rq[pr];
-          double gp = G[p * GLD + j], gq = G[q * GLD + j];
-          G[p * GLD + j] = c * gp - s * gq;
-          G[q * GLD + j] = s * gp + c * gq;
-        }
-      }
-      __syncthreads();
-      if (t < P2 / 2 && rs[t] != 0.0) {
-        int p = rp[t], q = rq[t];
-        G[p * GLD + q] = 0.0;
-        G[q * GLD + p] = 0.0;
-        s_any = 1;
-      }
-      __syncthreads();
-      any |= s_any;
-      __syncthreads();
-      if (t == 0) s_any = 0;
     }
-    if (!any) break;
+    if (!__syncthreads_or(any)) break;
   }
-  if (t == 0) *a.flag = 1;
-
-  // re-orthogonalise J (one Newton-Schulz step J <- J (3I - J^T J) / 2):
-  // hundreds of accumulated plane rotations drift O(n_rot * eps) from
-  // orthogonal, which would otherwise build up in V over the sweeps
-  {
-    double* E = G;  // G is no longer needed
-    __syncthreads();
-    for (int idx = t; idx < P2 * P2; idx += JT) {
-      int i = idx / P2, j = idx % P2;
-      double acc = 0.0;
-      for (int l = 0; l < P2; ++l) acc = fma(J[l * GLD + i], J[l * GLD + j], acc);
-      E[i * GLD + j] = acc - (i == j ? 1.0 : 0.0);
-    }
-    __syncthreads();
-    double nv[P2 * P2 / JT];
-#pragma unroll
-    for (int e = 0; e < P2 * P2 / JT; ++e) {
-      int idx = t + e * JT, i = idx / P2, j = idx % P2;
-      double acc = 0.0;
-      for (int l = 0; l < P2; ++l) acc = fma(J[i * GLD + l], E[l * GLD + j], acc);
-      nv[e] = J[i * GLD + j] - 0.5 * acc;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < P2 * P2 / JT; ++e) {
-      int idx = t + e * JT;
-      J[(idx / P2) * GLD + idx % P2] = nv[e];
-    }
-    __syncthreads();
+  // re-orthogonalise J: J <- J (3I - J^T J) / 2.  Hundreds of accumulated
+  // plane rotations drift O(n_rot * eps) from orthogonal, which would
+  // otherwise build up in V over the sweeps.
+  __syncthreads();
+  double* E = G;
+  for (int idx = t; idx < P2 * P2; idx += JT) {
+    int i = idx / P2, j = idx % P2;
+    double acc = 0.0;
+    for (int l = 0; l < P2; ++l) acc = fma(J[l * GLD + i], J[l * GLD + j], acc);
+    E[i * GLD + j] = acc - (i == j ? 1.0 : 0.0);
   }
+  __syncthreads();
+  double* Jout = a.J + (int64_t)pair * P2 * P2;
+  for (int idx = t; idx < P2 * P2; idx += JT) {
+    int i = idx / P2, j = idx % P2;
+    double acc = 0.0;
+    for (int l = 0; l < P2; ++l) acc = fma(J[i * GLD + l], E[l * GLD + j], acc);
+    Jout[idx] = J[i * GLD + j] - 0.5 * acc;
+  }
+}
 
-  // ---- 3. apply J to the X and V column blocks (DMMA) ----
-  // B fragments of J stay in registers: bj[ks][nt] = J[4ks + (lane&3)][8nt + (lane>>2)]
+__global__ void __launch_bounds__(JT) jacobi_apply_kernel(JacArgs a) {
+  __shared__ __align__(16) double buf[2][P2 * LDR];
+  const int pair = blockIdx.x;
+  if (a.skip[pair]) return;
+  const int which = blockIdx.y / a.splits, split = blockIdx.y % a.splits;
+  double* M = which == 0 ? a.X : a.V;
+  int bx, by;
+  pair_of_round(a.nb, a.round, pair, bx, by);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* Jg = a.J + (int64_t)pair * P2 * P2;
   double bj[8][4];
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) bj[ks][nt] = J[(4 * ks + (lane & 3)) * GLD + 8 * nt + (lane >> 2)];
-  for (int which = 0; which < 2; ++which) {
-    double* M = which == 0 ? a.X : a.V;
-    const int64_t ld = which == 0 ? a.ldx : a.ldv;
-    const int64_t rows = which == 0 ? a.rows : a.vrows;
-    for (int64_t r0 = 0; r0 < rows; r0 += CH) {
-      __syncthreads();
-      for (int idx = t; idx < CH * P2; idx += JT) {
-        int r = idx % CH, c = idx / CH;
-        int64_t gr = r0 + r;
-        chunk[r * CLD + c] = gr < rows ? M[gr + gcol(c, bx, by) * ld] : 0.0;
-      }
-      __syncthreads();
-      double o[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-      const double* arow = chunk + (8 * warp + (lane >> 2)) * CLD + (lane & 3);
+    for (int nt = 0; nt < 4; ++nt) bj[ks][nt] = Jg[(4 * ks + (lane & 3)) * P2 + 8 * nt + (lane >> 2)];
+  const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
+  const int nch = (int)cdiv_dev(re - rb, CH);
+  if (nch > 0) load_chunk(buf[0], M, a.ld, rb, re, bx, by);
+  cp_async_commit();
+  for (int i = 0; i < nch; ++i) {
+    if (i + 1 < nch) load_chunk(buf[(i + 1) & 1], M, a.ld, rb + (int64_t)(i + 1) * CH, re, bx, by);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    double* b = buf[i & 1];
+    // warp w: rows 8w..8w+7 of the chunk, all 32 columns (in place, warp-local)
+    double av[8];
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        double av = arow[4 * ks];
+    for (int ks = 0; ks < 8; ++ks) av[ks] = b[(4 * ks + (lane & 3)) * LDR + 8 * warp + (lane >> 2)];
+    double o[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma(o[nt], av, bj[ks][nt]);
-      }
-      __syncwarp();
-      double* orow = chunk + (8 * warp + (lane >> 2)) * CLD + 2 * (lane & 3);
+    for (int ks = 0; ks < 8; ++ks)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) { orow[8 * nt] = o[nt][0]; orow[8 * nt + 1] = o[nt][1]; }
-      __syncthreads();
-      for (int idx = t; idx < CH * P2; idx += JT) {
-        int r = idx % CH, c = idx / CH;
-        int64_t gr = r0 + r;
-        if (gr < rows) M[gr + gcol(c, bx, by) * ld] = chunk[r * CLD + c];
+      for (int nt = 0; nt < 4; ++nt) dmma(o[nt], av[ks], bj[ks][nt]);
+    __syncwarp();
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) b[(8 * nt + 2 * (lane & 3) + e) * LDR + 8 * warp + (lane >> 2)] = o[nt][e];
+    __syncthreads();
+    const int64_t r0 = rb + (int64_t)i * CH;
+    for (int s = threadIdx.x; s < NSEG; s += JT) {
+      const int c = s / (CH / 2), rp2 = s % (CH / 2);
+      const int64_t gr = r0 + 2 * rp2;
+      if (gr < re) {
+        double2 v = *reinterpret_cast<const double2*>(b + c * LDR + 2 * rp2);
+        *reinterpret_cast<double2*>(M + gr + gcol(c, bx, by) * a.ld) = v;
       }
     }
+    __syncthreads();
   }
 }
 
@@ -308,19 +371,19 @@ __global__ void gather_cols_kernel(const double* A, int64_t lda, int64_t rows, c
   }
 }
 
-// X (k x kp) = lower triangle source transposed: X[i][j] = R[j][i] for j <= i (R upper k x k)
+// X (kp x kp, zero padded) = R (upper, k x k) or R^T
 __global__ void tri_transpose_kernel(const double* R, int64_t ldr, int64_t k, int64_t kp,
                                      double* X, int upper) {
-  const int64_t total = k * kp;
+  const int64_t total = kp * kp;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = idx % k, j = idx / k;
+    int64_t i = idx % kp, j = idx / kp;
     double v = 0.0;
-    if (j < k) {
+    if (i < k && j < k) {
       if (upper) v = (i <= j) ? R[i + j * ldr] : 0.0;      // X = R
       else v = (j <= i) ? R[j + i * ldr] : 0.0;            // X = R^T
     }
-    X[i + j * k] = v;
+    X[idx] = v;
   }
 }
 
@@ -330,28 +393,72 @@ inline int gridn(int64_t n) {
 
 }  // namespace
 
-// Jacobi on the k x k matrix X (in place, ld = k, kp >= k padded columns
-// present and zero).  V (kp x kp) accumulates the rotations.  Returns sweeps.
+KernelProfile g_prof;
+
+// One-sided block Jacobi on the kp x kp matrix X (in place; columns >= k
+// and rows >= k are zero).  V (kp x kp) accumulates the rotations.
 static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, double* V) {
   set_identity(st, kp, kp, V, kp);
-  const int nb = (int)(kp / JB);
+  const int nb = (int)(kp / JB), npairs = nb / 2;
   const double eps = 2.220446049250313e-16;
   const double tol = 8.0 * eps * sqrt((double)std::max<int64_t>(k, 1));
-  DBuf<int> flag(1, st);
+  int splits = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(592, npairs)), cdiv(kp, CH));
+  int64_t rps = cdiv(cdiv(kp, splits), CH) * CH;
+  splits = (int)cdiv(kp, rps);
+  DBuf<double> gpart((size_t)npairs * splits * P2 * P2, st), J((size_t)npairs * P2 * P2, st);
+  DBuf<int> skip(npairs, st), flag(1, st);
+  static const int inner = std::getenv("MPO_B200_INNER") ? std::atoi(std::getenv("MPO_B200_INNER")) : 1;
+  JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), J.get(), skip.get(), flag.get(), tol,
+            inner, nullptr};
+  // profiling (bench.py roofline): CUDA events around every round kernel
+  const bool prof = g_prof.on;
+  DBuf<int> skiplog;
+  std::vector<cudaEvent_t> ev;
+  if (prof) {
+    skiplog.alloc((size_t)(nb - 1) * npairs, st);
+    a.skiplog = skiplog.get();
+    ev.resize(4 * (nb - 1));
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+  }
   int h_flag = 0, sweeps = 0;
   for (int sweep = 0; sweep < 60; ++sweep) {
     CK(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
     for (int r = 0; r < nb - 1; ++r) {
-      RoundArgs a{X, k, k, V, kp, kp, nb, r, tol, flag.get()};
-      jacobi_round_kernel<<<nb / 2, JT, 0, st>>>(a);
+      a.round = r;
+      if (prof) CK(cudaEventRecord(ev[4 * r], st));
+      jacobi_gram_kernel<<<dim3(npairs, splits), JT, 0, st>>>(a);
       CK_LAUNCH();
+      if (prof) CK(cudaEventRecord(ev[4 * r + 1], st));
+      jacobi_eig_kernel<<<npairs, JT, 0, st>>>(a);
+      CK_LAUNCH();
+      if (prof) CK(cudaEventRecord(ev[4 * r + 2], st));
+      jacobi_apply_kernel<<<dim3(npairs, 2 * splits), JT, 0, st>>>(a);
+      CK_LAUNCH();
+      if (prof) CK(cudaEventRecord(ev[4 * r + 3], st));
     }
-    note_launch(nb - 1);
+    note_launch(3 * (nb - 1));
     CK(cudaMemcpyAsync(&h_flag, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (prof) {
+      std::vector<int> sk((size_t)(nb - 1) * npairs);
+      CK(cudaMemcpy(sk.data(), skiplog.get(), sizeof(int) * sk.size(), cudaMemcpyDeviceToHost));
+      for (int r = 0; r < nb - 1; ++r) {
+        float t0, t1, t2;
+        CK(cudaEventElapsedTime(&t0, ev[4 * r], ev[4 * r + 1]));
+        CK(cudaEventElapsedTime(&t1, ev[4 * r + 1], ev[4 * r + 2]));
+        CK(cudaEventElapsedTime(&t2, ev[4 * r + 2], ev[4 * r + 3]));
+        int active = 0;
+        for (int p = 0; p < npairs; ++p) active += sk[(size_t)r * npairs + p] == 0;
+        const double unit = 2.0 * (double)kp * P2 * P2;  // one 32-column block of one matrix
+        g_prof.add(0, t0, unit * npairs);
+        g_prof.add(1, t1, 0.0);
+        g_prof.add(2, t2, 2.0 * unit * active);
+      }
+    }
     ++sweeps;
     if (!h_flag) break;
   }
+  for (auto& e : ev) cudaEventDestroy(e);
   return sweeps;
 }
 
@@ -376,15 +483,22 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
     copy_matrix(st, m, n, M, ldm, A.get(), m);
   }
   householder_qr(st, tm, k, A.get(), tm, Q.get(), tm, R.get(), k);
-  // X = T^T (wide) or T (tall), padded to kp columns
-  DBuf<double> X((size_t)k * kp, st), V((size_t)kp * kp, st);
-  tri_transpose_kernel<<<gridn(k * kp), 256, 0, st>>>(R.get(), k, k, kp, X.get(), wide ? 0 : 1);
+  // X = T^T (wide) or T (tall), zero padded to kp x kp
+  DBuf<double> X((size_t)kp * kp, st), V((size_t)kp * kp, st);
+  tri_transpose_kernel<<<gridn(kp * kp), 256, 0, st>>>(R.get(), k, k, kp, X.get(), wide ? 0 : 1);
   CK_LAUNCH();
   note_launch();
-  jacobi_sweeps(st, X.get(), k, kp, V.get());
+  static const bool trace = std::getenv("MPO_B200_TRACE") != nullptr;
+  if (trace) CK(cudaStreamSynchronize(st));
+  auto t0 = std::chrono::steady_clock::now();
+  const int sweeps = jacobi_sweeps(st, X.get(), k, kp, V.get());
+  if (trace) {
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[mpo_b200]   jacobi k=%lld sweeps=%d %.3f ms\n", (long long)k, sweeps, ms);
+  }
   // singular values = column norms, sorted
   DBuf<double> norms(kp, st);
-  col_norms_kernel<<<(int)cdiv(kp, 8), 256, 0, st>>>(X.get(), k, k, kp, norms.get());
+  col_norms_kernel<<<(int)cdiv(kp, 8), 256, 0, st>>>(X.get(), kp, kp, kp, norms.get());
   CK_LAUNCH();
   int np2 = 1;
   while (np2 < kp) np2 <<= 1;
@@ -398,9 +512,9 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   CK_LAUNCH();
   CK(cudaMemcpyAsync(out.s.get(), norms.get(), sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
   note_launch(2);
-  // sorted Y = X[:, perm] (k x k) and Vs = V[0:k, perm]
+  // sorted Y = X[0:k, perm] and Vs = V[0:k, perm]
   DBuf<double> Ys((size_t)k * k, st), Vs((size_t)k * k, st);
-  gather_cols_kernel<<<gridn(k * k), 256, 0, st>>>(X.get(), k, k, perm.get(), k, Ys.get(), k);
+  gather_cols_kernel<<<gridn(k * k), 256, 0, st>>>(X.get(), kp, k, perm.get(), k, Ys.get(), k);
   CK_LAUNCH();
   gather_cols_kernel<<<gridn(k * k), 256, 0, st>>>(V.get(), kp, k, perm.get(), k, Vs.get(), k);
   CK_LAUNCH();
@@ -420,10 +534,6 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   }
 }
 
-}  // namespace mpob
-
-namespace mpob {
-
 namespace {
 
 // W[:, j] = Ucarry[:, j] / s_j; columns with s_j == 0 are completed to an
@@ -434,6 +544,7 @@ __global__ void left_vectors_kernel(int k, const double* U, int64_t ldu, const d
   __shared__ double red[32];
   __shared__ int s_ok;
   const int t = threadIdx.x;
+  const int nw = (int)(blockDim.x >> 5);
   for (int j = 0; j < k; ++j) {
     double sj = s[j];
     if (sj > 0.0) {
@@ -453,7 +564,7 @@ __global__ void left_vectors_kernel(int k, const double* U, int64_t ldu, const d
           for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
           if ((t & 31) == 0) red[t >> 5] = d;
           __syncthreads();
-          if (t == 0) { double a = 0; for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w]; red[0] = a; }
+          if (t == 0) { double acc = 0; for (int w = 0; w < nw; ++w) acc += red[w]; red[0] = acc; }
           __syncthreads();
           d = red[0];
           __syncthreads();
@@ -466,7 +577,7 @@ __global__ void left_vectors_kernel(int k, const double* U, int64_t ldu, const d
       for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
       if ((t & 31) == 0) red[t >> 5] = nn;
       __syncthreads();
-      if (t == 0) { double a = 0; for (int w = 0; w < (int)(blockDim.x >> 5); ++w) a += red[w]; red[0] = sqrt(a); }
+      if (t == 0) { double acc = 0; for (int w = 0; w < nw; ++w) acc += red[w]; red[0] = sqrt(acc); }
       __syncthreads();
       double nrm = red[0];
       if (nrm > 0.5) {

@@ -179,6 +179,29 @@ def tnrsvd(a, k_target: int, q: int = 2, round_tol: float | None = DEFAULT_ROUND
     return LowRankSvd(u=u, s=s, v=v, k_target=int(k_target), k_oversampled=kk)
 
 
+def prepare(a, k_target: int, oversample: float = 2.0, seed=None):
+    """Device-resident inputs of one TNrSVD: the merged operator and the
+    sketch (rsvd.py:235-244), so a timed step starts with both in HBM."""
+    kk = sketch_width(k_target, oversample)
+    cnt = merge_count(a.row_dims, a.col_dims, kk)
+    da, _ = _dev(a if isinstance(a, DeviceMpo) else a.densify())
+    am = merge_leading_cores(da, cnt) if cnt > 1 else da
+    o = DeviceMpo.from_host(random_unit_rank_mpo(_merged_col_dims(a.col_dims, cnt), kk, seed))
+    return am, o, kk
+
+
+def tnrsvd_prepared(am: DeviceMpo, o: DeviceMpo, k_target: int, q: int = 2,
+                    round_tol: float | None = DEFAULT_ROUND_TOL):
+    """The device pipeline of rsvd.py:244-259 on prepared inputs; returns
+    (U, s, V) with U, V resident in HBM."""
+    s = np.zeros(k_target, dtype=np.float64)
+    hu, hv = C.c_void_p(), C.c_void_p()
+    tol, has = _tol(round_tol)
+    _lib.call("mpo_tnrsvd", am.ctx, am.handle, o.handle, int(k_target), int(q), tol, has,
+              C.byref(hu), s.ctypes.data_as(_lib._DP), C.byref(hv))
+    return DeviceMpo(hu, am.ctx), s, DeviceMpo(hv, am.ctx)
+
+
 def reconstruct_matrix(lr: LowRankSvd, guard: int | None = None) -> np.ndarray:
     """Dense U diag(s) V^T (desk-scale verification helper)."""
     g = CONTRACT_GUARD if guard is None else guard
