@@ -487,9 +487,9 @@ def gram_first_index(x, y):
         cx2 = cx.reshape(cx.shape[0], -1, cx.shape[3], order="F")
         cy2 = cy.reshape(cy.shape[0], -1, cy.shape[3], order="F")
         if t is None:
-            t = np.einsum("aib,cib->ac", cx2, cy2)
+            t = np.tensordot(cx2, cy2, axes=([1, 2], [1, 2]))
         else:
-            t = np.einsum("aib,bd,cid->ac", cx2, t, cy2)
+            t = np.tensordot(np.tensordot(cx2, t, axes=(2, 0)), cy2, axes=([1, 2], [1, 2]))
     c0x, c0y = x[0][0], y[0][0]        # (I1, K, R)
     if t is None:
         return np.einsum("ikr,ilr->kl", c0x, c0y)

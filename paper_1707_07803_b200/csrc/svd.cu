@@ -188,13 +188,16 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
         pair_of_round(P2, r, 2 * warp + u, p, q);
         if (p > q) { int tmp = p; p = q; q = tmp; }
         const double gpp = G[p * GLD + p], gqq = G[q * GLD + q], gpq = G[p * GLD + q];
-        const double dd = sqrt(gpp) * sqrt(gqq);
-        rot[u] = dd > 0.0 && fabs(gpq) > a.tol * dd;
+        // |gpq| > tol sqrt(gpp gqq), with independent rsqrts (no underflow of gpp*gqq)
+        rot[u] = gpp > 0.0 && gqq > 0.0 && fabs(gpq) * rsqrt(gpp) * rsqrt(gqq) > a.tol;
         double c = 1.0, s = 0.0, tt = 0.0;
         if (rot[u]) {
-          const double zeta = (gqq - gpp) / (2.0 * gpq);
-          tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          c = 1.0 / sqrt(1.0 + tt * tt);
+          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (gqq - gpp) / (2 gpq),
+          // rewritten with one sqrt and one division on the critical path
+          const double d = gqq - gpp, g2 = 2.0 * fabs(gpq);
+          const double sg = (d == 0.0) ? 1.0 : ((d > 0.0) == (gpq > 0.0) ? 1.0 : -1.0);
+          tt = sg * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
+          c = rsqrt(fma(tt, tt, 1.0));
           s = tt * c;
         }
         pp[u] = p; qq[u] = q; cc[u] = c; ss[u] = s;
