@@ -45,6 +45,32 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// dlarft (forward, columnwise) in shared memory, one column per step with
+// the i < j entries in parallel: T(0:j, j) = -tau_j T(0:j,0:j) S(0:j, j),
+// S = V^T V (strict upper part used).  Writes T (w x w, column-major) and
+// tau to global memory.  Called by all threads of one CTA.
+__device__ void build_t_factor(const double* S, double* sT, const double* tau_in, int w,
+                               double* T, double* tau_out) {
+  const int t = threadIdx.x;
+  for (int j = 0; j < w; ++j) {
+    const double tj = tau_in[j];
+    if (t < w) {
+      double v;
+      if (t < j) {
+        double acc = 0.0;
+        for (int l = t; l < j; ++l) acc = fma(sT[t + l * w], S[l + j * w], acc);
+        v = -tj * acc;
+      } else {
+        v = (t == j) ? tj : 0.0;
+      }
+      sT[t + j * w] = v;
+    }
+    __syncthreads();
+  }
+  for (int idx = t; idx < w * w; idx += blockDim.x) T[idx] = sT[idx];
+  for (int idx = t; idx < w; idx += blockDim.x) tau_out[idx] = tau_in[idx];
+}
+
 __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(PanelArgs p) {
   extern __shared__ double chunk[];  // rpc x w, column-major: chunk[r + col*ld]
   __shared__ double red[QR_THREADS / 32];
@@ -164,26 +190,17 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(PanelArgs p) {
   grid.sync();
   if (c == 0) {
     // dlarft (forward, columnwise): T(0:j, j) = -tau_j T(0:j,0:j) V(:,0:j)^T v_j
-    double* T = p.T;
     __shared__ double sv[QR_NB * QR_NB];
+    __shared__ double st_[QR_NB * QR_NB];
+    __shared__ double stau[QR_NB];
     for (int idx = t; idx < w * w; idx += QR_THREADS) {
       double tot = 0.0;
       for (int i = 0; i < G; ++i) tot += p.vtv[(int64_t)i * w * w + idx];
       sv[idx] = tot;  // sv[a + b*w] = v_a . v_b (a < b)
     }
+    for (int idx = t; idx < w; idx += QR_THREADS) stau[idx] = p.tau[idx];
     __syncthreads();
-    if (t == 0) {
-      for (int j = 0; j < w; ++j) {
-        double tj = p.tau[j];
-        for (int i = 0; i < j; ++i) {
-          double acc = 0.0;
-          for (int l = i; l < j; ++l) acc += T[i + l * w] * sv[l + j * w];
-          T[i + j * w] = -tj * acc;
-        }
-        T[j + j * w] = tj;
-        for (int i = j + 1; i < w; ++i) T[i + j * w] = 0.0;
-      }
-    }
+    build_t_factor(sv, st_, stau, w, p.T, p.tau);
   }
 }
 
@@ -319,20 +336,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
       chunk[idx] = tot;  // reuse own chunk (already written back)
     }
     __syncthreads();
-    if (t == 0) {
-      double* T = p.T;
-      for (int j = 0; j < w; ++j) {
-        const double tj = s_tau[j];
-        p.tau[j] = tj;
-        for (int i = 0; i < j; ++i) {
-          double acc = 0.0;
-          for (int l = i; l < j; ++l) acc += T[i + l * w] * chunk[l + j * w];
-          T[i + j * w] = -tj * acc;
-        }
-        T[j + j * w] = tj;
-        for (int i = j + 1; i < w; ++i) T[i + j * w] = 0.0;
-      }
-    }
+    build_t_factor(chunk, chunk + w * w, s_tau, w, p.T, p.tau);  // rpc >= 64 >= 2w
   }
   cluster.sync();  // keep every CTA's shared memory alive until rank 0 is done
 }

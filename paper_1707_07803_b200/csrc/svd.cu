@@ -95,6 +95,7 @@ struct JacArgs {
   double tol;
   int inner;       // max inner (32 x 32 Gram) Jacobi sweeps per outer round
   int* skiplog;    // profiling only: per (round, pair) skip flags, or null
+  long long* dbg;  // MPO_B200_EIGDBG: clock64 phase counters of pair 0, or null
 };
 
 __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
@@ -139,12 +140,34 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
   __shared__ double J[P2 * GLD];
   __shared__ int s_skip;
   const int t = threadIdx.x, pair = blockIdx.x;
-  for (int idx = t; idx < P2 * P2; idx += JT) {
-    const double* gp = a.gpart + (int64_t)pair * a.splits * (P2 * P2) + idx;
-    double s = 0.0;
-    for (int sp = 0; sp < a.splits; ++sp) s += gp[(int64_t)sp * P2 * P2];
-    G[(idx / P2) * GLD + idx % P2] = s;
-    J[(idx / P2) * GLD + idx % P2] = (idx / P2 == idx % P2) ? 1.0 : 0.0;
+  {
+    // sum the row-split partial Grams in split order (loads issued first)
+    constexpr int PER = P2 * P2 / JT;
+    const double* gp = a.gpart + (int64_t)pair * a.splits * (P2 * P2) + t;
+    double s[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) s[e] = 0.0;
+    int sp = 0;
+    for (; sp + 4 <= a.splits; sp += 4) {
+      double v[4][PER];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < PER; ++e) v[q][e] = gp[(int64_t)(sp + q) * P2 * P2 + e * JT];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < PER; ++e) s[e] += v[q][e];
+    }
+    for (; sp < a.splits; ++sp)
+#pragma unroll
+      for (int e = 0; e < PER; ++e) s[e] += gp[(int64_t)sp * P2 * P2 + e * JT];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int idx = t + e * JT;
+      G[(idx / P2) * GLD + idx % P2] = s[e];
+      J[(idx / P2) * GLD + idx % P2] = (idx / P2 == idx % P2) ? 1.0 : 0.0;
+    }
   }
   if (t == 0) s_skip = 1;
   __syncthreads();
@@ -170,99 +193,168 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
   if (s_skip) return;
   if (t == 0) *a.flag = 1;
 
-  // cyclic two-sided Jacobi on G (parallel circle ordering).  Warp w owns
-  // pairs 2w and 2w+1 of every round: it computes their rotations
-  // redundantly in all lanes, then updates the pairs' columns (lane = row)
-  // and, after a CTA barrier, their rows (lane = column); two barriers per
-  // round, no shared rotation tables.
-  const int lane = t & 31, warp = t >> 5;
+  // cyclic two-sided Jacobi on G (parallel circle ordering), three short
+  // phases per round: 16 lanes compute the round's 16 rotations, then all
+  // threads update the rotated columns of G and J, then the rotated rows of
+  // G (folding in the exact 2x2 results).  Rotation parameters are seeded in
+  // FP32 (MUFU rsqrt / rcp, scale-free operands) and renormalised in FP64
+  // so that c^2 + s^2 = 1 to FP64 rounding; the angle is thereby accurate to
+  // ~1e-7 relative, which only affects how much of |gpq| one rotation
+  // removes, never the orthogonality of J.  The FP64 sweep test and the
+  // fresh FP64 Gram of every outer round decide convergence.
+  __shared__ unsigned char s_pq[P2 - 1][P2 / 2][2];
+  __shared__ double rc[P2 / 2], rs[P2 / 2], rdp[P2 / 2], rdq[P2 / 2];
+  __shared__ int rflag[P2 / 2];
+  for (int idx = t; idx < (P2 - 1) * (P2 / 2); idx += JT) {
+    int r = idx / (P2 / 2), i = idx % (P2 / 2), p, q;
+    pair_of_round(P2, r, i, p, q);
+    s_pq[r][i][0] = (unsigned char)min(p, q);
+    s_pq[r][i][1] = (unsigned char)max(p, q);
+  }
+  __syncthreads();
+  long long c_rot = 0, c_col = 0, c_row = 0, c0 = clock64();
   for (int sweep = 0; sweep < a.inner; ++sweep) {
     int any = 0;
     for (int r = 0; r < P2 - 1; ++r) {
-      int pp[2], qq[2];
-      double cc[2], ss[2], dp[2], dq[2];
-      bool rot[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        int p, q;
-        pair_of_round(P2, r, 2 * warp + u, p, q);
-        if (p > q) { int tmp = p; p = q; q = tmp; }
+      long long cr = clock64();
+      if (t < P2 / 2) {
+        const int p = s_pq[r][t][0], q = s_pq[r][t][1];
         const double gpp = G[p * GLD + p], gqq = G[q * GLD + q], gpq = G[p * GLD + q];
-        // |gpq| > tol sqrt(gpp gqq), with independent rsqrts (no underflow of gpp*gqq)
-        rot[u] = gpp > 0.0 && gqq > 0.0 && fabs(gpq) * rsqrt(gpp) * rsqrt(gqq) > a.tol;
-        double c = 1.0, s = 0.0, tt = 0.0;
-        if (rot[u]) {
-          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (gqq - gpp) / (2 gpq),
-          // rewritten with one sqrt and one division on the critical path
+        // |gpq| > tol sqrt(gpp gqq) without FP64 rsqrt on the critical path;
+        // the product form is exact unless gpp*gqq underflows (graded columns)
+        const double pq = gpp * gqq;
+        const bool rot = gpp > 0.0 && gqq > 0.0 &&
+                         (pq > 1e-280 ? gpq * gpq > a.tol * a.tol * pq
+                                      : fabs(gpq) * rsqrt(gpp) * rsqrt(gqq) > a.tol);
+        double c = 1.0, s = 0.0;
+        if (rot) {
           const double d = gqq - gpp, g2 = 2.0 * fabs(gpq);
+          const double mx = fmax(fabs(d), g2);
+          float df, gf;
+          if (mx > 1e-18 && mx < 1e18) {          // common case: plain conversion
+            df = (float)fabs(d);
+            gf = (float)g2;
+          } else {                                // exact power-of-two rescale
+            const double sc = scalbn(1.0, -ilogb(mx));
+            df = (float)(fabs(d) * sc);
+            gf = (float)(g2 * sc);
+          }
+          // MUFU approximations only (rsqrt, reciprocal): ~1e-7 relative
+          const float r2 = fmaf(df, df, gf * gf);
+          const float tf = __fdividef(gf, df + r2 * rsqrtf(r2));
+          const float cf = rsqrtf(fmaf(tf, tf, 1.0f));
           const double sg = (d == 0.0) ? 1.0 : ((d > 0.0) == (gpq > 0.0) ? 1.0 : -1.0);
-          tt = sg * g2 / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
-          c = rsqrt(fma(tt, tt, 1.0));
-          s = tt * c;
+          c = (double)cf;
+          s = sg * (double)tf * (double)cf;
+          const double f = 1.5 - 0.5 * fma(c, c, s * s);   // one Newton step: c^2+s^2 -> 1
+          c *= f;
+          s *= f;
         }
-        pp[u] = p; qq[u] = q; cc[u] = c; ss[u] = s;
-        dp[u] = gpp - tt * gpq;   // exact-formula diagonal after the rotation
-        dq[u] = gqq + tt * gpq;
-        any |= rot[u];
-      }
-      __syncwarp();
-      // columns p, q of G and J: (col_p, col_q) <- (c col_p - s col_q, s col_p + c col_q)
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (!rot[u]) continue;
-        const int p = pp[u], q = qq[u];
-        const double c = cc[u], s = ss[u];
-        const double gp = G[lane * GLD + p], gq = G[lane * GLD + q];
-        G[lane * GLD + p] = c * gp - s * gq;
-        G[lane * GLD + q] = s * gp + c * gq;
-        const double jp = J[lane * GLD + p], jq = J[lane * GLD + q];
-        J[lane * GLD + p] = c * jp - s * jq;
-        J[lane * GLD + q] = s * jp + c * jq;
+        rc[t] = c; rs[t] = s; rflag[t] = rot;
+        // diagonal after the rotation (same c, s as the G update below)
+        rdp[t] = fma(c * c, gpp, fma(-2.0 * c * s, gpq, s * s * gqq));
+        rdq[t] = fma(s * s, gpp, fma(2.0 * c * s, gpq, c * c * gqq));
+        any |= rot;
       }
       __syncthreads();
+      long long cc1 = clock64();
+      c_rot += cc1 - cr;
+      // one phase: thread (u, v) owns the 2x2 block G[{p_u,q_u}, {p_v,q_v}]
+      // and forms R_u^T B R_v in registers (no intra-phase dependencies);
+      // the same threads rotate columns p_v, q_v of J (two rows each)
+      {
+        const int u = t / (P2 / 2), v = t % (P2 / 2);
+        const int pu = s_pq[r][u][0], qu = s_pq[r][u][1];
+        const int pv = s_pq[r][v][0], qv = s_pq[r][v][1];
+        const double cu = rc[u], su = rs[u], cv = rc[v], sv = rs[v];
+        if (u == v) {
+          if (rflag[u]) {
+            G[pu * GLD + pu] = rdp[u];
+            G[qu * GLD + qu] = rdq[u];
+            G[pu * GLD + qu] = 0.0;
+            G[qu * GLD + pu] = 0.0;
+          }
+        } else if (rflag[u] | rflag[v]) {
+          const double b00 = G[pu * GLD + pv], b01 = G[pu * GLD + qv];
+          const double b10 = G[qu * GLD + pv], b11 = G[qu * GLD + qv];
+          // B R_v (columns), then R_u^T (rows)
+          const double x00 = cv * b00 - sv * b01, x01 = sv * b00 + cv * b01;
+          const double x10 = cv * b10 - sv * b11, x11 = sv * b10 + cv * b11;
+          G[pu * GLD + pv] = cu * x00 - su * x10;
+          G[pu * GLD + qv] = cu * x01 - su * x11;
+          G[qu * GLD + pv] = su * x00 + cu * x10;
+          G[qu * GLD + qv] = su * x01 + cu * x11;
+        }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (!rot[u]) continue;
-        const int p = pp[u], q = qq[u];
-        const double c = cc[u], s = ss[u];
-        const double gp = G[p * GLD + lane], gq = G[q * GLD + lane];
-        G[p * GLD + lane] = c * gp - s * gq;
-        G[q * GLD + lane] = s * gp + c * gq;
-      }
-      __syncwarp();
-      if (lane == 0) {
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (!rot[u]) continue;
-          G[pp[u] * GLD + qq[u]] = 0.0;
-          G[qq[u] * GLD + pp[u]] = 0.0;
-          G[pp[u] * GLD + pp[u]] = dp[u];
-          G[qq[u] * GLD + qq[u]] = dq[u];
+        for (int h = 0; h < 2; ++h) {
+          const int idx = t + h * JT, w = idx / P2, row = idx % P2;
+          if (rflag[w]) {
+            const int p = s_pq[r][w][0], q = s_pq[r][w][1];
+            const double c = rc[w], s = rs[w];
+            const double jp = J[row * GLD + p], jq = J[row * GLD + q];
+            J[row * GLD + p] = c * jp - s * jq;
+            J[row * GLD + q] = s * jp + c * jq;
+          }
         }
       }
       __syncthreads();
+      c_col += clock64() - cc1;
     }
     if (!__syncthreads_or(any)) break;
   }
-  // re-orthogonalise J: J <- J (3I - J^T J) / 2.  Hundreds of accumulated
-  // plane rotations drift O(n_rot * eps) from orthogonal, which would
-  // otherwise build up in V over the sweeps.
-  __syncthreads();
+  if (a.dbg && pair == 0 && t == 0) {
+    a.dbg[0] = c_rot; a.dbg[1] = c_col; a.dbg[2] = c_row; a.dbg[3] = clock64() - c0;
+  }
+  // re-orthogonalise J: two Newton-Schulz steps J <- J - J (J^T J - I) / 2
+  // (each squares the orthogonality defect of the accumulated rotations);
+  // the 32 x 32 x 32 products run on the DMMA pipe, two 8x8 tiles per warp
   double* E = G;
-  for (int idx = t; idx < P2 * P2; idx += JT) {
-    int i = idx / P2, j = idx % P2;
-    double acc = 0.0;
-    for (int l = 0; l < P2; ++l) acc = fma(J[l * GLD + i], J[l * GLD + j], acc);
-    E[i * GLD + j] = acc - (i == j ? 1.0 : 0.0);
+  const int lane = t & 31, warp = t >> 5;
+  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
+  for (int it = 0; it < 2; ++it) {
+    __syncthreads();
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int k0 = 0; k0 < P2; k0 += 4) {
+      const int kk = k0 + (lane & 3);
+      const double av = J[kk * GLD + ti * 8 + (lane >> 2)];          // (J^T)[i][k]
+      dmma(acc[0], av, J[kk * GLD + tj0 * 8 + (lane >> 2)]);
+      dmma(acc[1], av, J[kk * GLD + (tj0 + 1) * 8 + (lane >> 2)]);
+    }
+    {
+      const int gi = ti * 8 + (lane >> 2);
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int gj = (tj0 + u) * 8 + 2 * (lane & 3) + e;
+          E[gi * GLD + gj] = acc[u][e] - (gi == gj ? 1.0 : 0.0);
+        }
+    }
+    __syncthreads();
+    double nv[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int k0 = 0; k0 < P2; k0 += 4) {
+      const int kk = k0 + (lane & 3);
+      const double av = J[(ti * 8 + (lane >> 2)) * GLD + kk];        // J[i][k]
+      dmma(nv[0], av, E[kk * GLD + tj0 * 8 + (lane >> 2)]);
+      dmma(nv[1], av, E[kk * GLD + (tj0 + 1) * 8 + (lane >> 2)]);
+    }
+    __syncthreads();
+    {
+      const int gi = ti * 8 + (lane >> 2);
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int gj = (tj0 + u) * 8 + 2 * (lane & 3) + e;
+          J[gi * GLD + gj] -= 0.5 * nv[u][e];
+        }
+    }
   }
   __syncthreads();
   double* Jout = a.J + (int64_t)pair * P2 * P2;
-  for (int idx = t; idx < P2 * P2; idx += JT) {
-    int i = idx / P2, j = idx % P2;
-    double acc = 0.0;
-    for (int l = 0; l < P2; ++l) acc = fma(J[i * GLD + l], E[l * GLD + j], acc);
-    Jout[idx] = J[i * GLD + j] - 0.5 * acc;
-  }
+  for (int idx = t; idx < P2 * P2; idx += JT) Jout[idx] = J[(idx / P2) * GLD + idx % P2];
 }
 
 __global__ void __launch_bounds__(JT) jacobi_apply_kernel(JacArgs a) {
@@ -374,6 +466,28 @@ __global__ void gather_cols_kernel(const double* A, int64_t lda, int64_t rows, c
   }
 }
 
+// dst[perm[i], j] = src[i, j]
+__global__ void scatter_rows_kernel(const double* src, int64_t lds, int64_t rows, int64_t cols,
+                                    const int* perm, double* dst, int64_t ldd) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = idx % rows, j = idx / rows;
+    dst[(int64_t)perm[i] + j * ldd] = src[i + j * lds];
+  }
+}
+
+// dst[i, perm[j]] = src[i, j]
+__global__ void scatter_cols_kernel(const double* src, int64_t lds, int64_t rows, int64_t cols,
+                                    const int* perm, double* dst, int64_t ldd) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = idx % rows, j = idx / rows;
+    dst[i + (int64_t)perm[j] * ldd] = src[i + j * lds];
+  }
+}
+
 // X (kp x kp, zero padded) = R (upper, k x k) or R^T
 __global__ void tri_transpose_kernel(const double* R, int64_t ldr, int64_t k, int64_t kp,
                                      double* X, int upper) {
@@ -412,7 +526,14 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   DBuf<int> skip(npairs, st), flag(1, st);
   static const int inner = std::getenv("MPO_B200_INNER") ? std::atoi(std::getenv("MPO_B200_INNER")) : 1;
   JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), J.get(), skip.get(), flag.get(), tol,
-            inner, nullptr};
+            inner, nullptr, nullptr};
+  static const bool eigdbg = std::getenv("MPO_B200_EIGDBG") != nullptr;
+  DBuf<long long> dbg;
+  if (eigdbg) {
+    dbg.alloc(4, st);
+    CK(cudaMemsetAsync(dbg.get(), 0, 4 * sizeof(long long), st));
+    a.dbg = dbg.get();
+  }
   // profiling (bench.py roofline): CUDA events around every round kernel
   const bool prof = g_prof.on;
   DBuf<int> skiplog;
@@ -459,6 +580,12 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
       }
     }
     ++sweeps;
+    if (eigdbg) {
+      long long hd[4];
+      CK(cudaMemcpy(hd, dbg.get(), sizeof(hd), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[mpo_b200] eig k=%lld sweep %d clocks: rot %lld col %lld row %lld total %lld\n",
+              (long long)k, sweeps, hd[0], hd[1], hd[2], hd[3]);
+    }
     if (!h_flag) break;
   }
   for (auto& e : ev) cudaEventDestroy(e);
@@ -484,6 +611,30 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
     }
   } else {
     copy_matrix(st, m, n, M, ldm, A.get(), m);
+  }
+  // pre-pivoting: order the tall orientation's columns by decreasing norm
+  // before the QR (a cheap stand-in for QR with column pivoting, which
+  // grades T's diagonal and shortens the Jacobi iteration)
+  static const bool presort = !std::getenv("MPO_B200_NOPRESORT");
+  DBuf<int> cperm;
+  if (presort && k > 1) {
+    int np2c = 1;
+    while (np2c < k) np2c <<= 1;
+    if (np2c <= 8192) {
+      DBuf<double> cn(k, st), A2((size_t)tm * k, st);
+      cperm.alloc(k, st);
+      col_norms_kernel<<<(int)cdiv(k, 8), 256, 0, st>>>(A.get(), tm, tm, k, cn.get());
+      CK_LAUNCH();
+      const size_t sm = (size_t)np2c * (sizeof(double) + sizeof(int));
+      if (sm > 48 * 1024)
+        CK(cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      sort_desc_kernel<<<1, 1024, sm, st>>>(cn.get(), (int)k, np2c, cn.get(), cperm.get());
+      CK_LAUNCH();
+      gather_cols_kernel<<<gridn(tm * k), 256, 0, st>>>(A.get(), tm, tm, cperm.get(), k, A2.get(), tm);
+      CK_LAUNCH();
+      note_launch(3);
+      A = std::move(A2);
+    }
   }
   householder_qr(st, tm, k, A.get(), tm, Q.get(), tm, R.get(), k);
   // X = T^T (wide) or T (tall), zero padded to kp x kp
@@ -525,15 +676,30 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   out.ucarry.alloc((size_t)m * k, st);
   out.vh.alloc((size_t)k * n, st);
   if (wide) {
-    // M = X Q^T, X Vs = Ys:  Ucarry = Ys (m = k rows),  Vh = Vs^T Q^T = (Q Vs)^T
-    copy_matrix(st, k, k, Ys.get(), k, out.ucarry.get(), m);
+    // P^T M = X Q^T, X Vs = Ys:  Ucarry = P Ys (m = k rows),  Vh = (Q Vs)^T
+    if (cperm.size())
+      scatter_rows_kernel<<<gridn(k * k), 256, 0, st>>>(Ys.get(), k, k, k, cperm.get(),
+                                                         out.ucarry.get(), m);
+    else
+      copy_matrix(st, k, k, Ys.get(), k, out.ucarry.get(), m);
     dgemm(st, true, true, k, n, k, 1.0, Vs.get(), k, Q.get(), tm, 0.0, out.vh.get(), k);
   } else {
-    // M = Q X:  Ucarry = Q Ys,  Vh = Vs^T
+    // M P = Q X:  Ucarry = Q Ys,  Vh = Vs^T P^T
     dgemm(st, false, false, m, k, k, 1.0, Q.get(), tm, Ys.get(), k, 0.0, out.ucarry.get(), m);
     int64_t dims[2] = {k, k};
     int pr[2] = {1, 0};
-    permute(st, Vs.get(), out.vh.get(), 2, dims, pr);
+    if (cperm.size()) {
+      DBuf<double> vt((size_t)k * k, st);
+      permute(st, Vs.get(), vt.get(), 2, dims, pr);
+      scatter_cols_kernel<<<gridn(k * k), 256, 0, st>>>(vt.get(), k, k, k, cperm.get(),
+                                                         out.vh.get(), k);
+    } else {
+      permute(st, Vs.get(), out.vh.get(), 2, dims, pr);
+    }
+  }
+  if (cperm.size()) {
+    CK_LAUNCH();
+    note_launch();
   }
 }
 
