@@ -144,6 +144,34 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs g) {
     return;
   }
   double* C = g.C + bat * g.sC;
+  // all C reads are issued before any C write (the compiler cannot prove the
+  // addresses distinct, so an interleaved read-modify-write would serialise
+  // on the full memory latency of every element)
+  if (g.beta != 0.0) {
+    double old[4][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          int64_t gi = m0 + wm * 32 + mi * 8 + row, gj = n0 + wn * 32 + ni * 8 + col + e;
+          old[mi][ni][e] = (gi < g.m && gj < g.n) ? __ldcg(C + gi + gj * g.ldc) : 0.0;
+        }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[mi][ni][e] = g.alpha * acc[mi][ni][e] + g.beta * old[mi][ni][e];
+  } else {
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[mi][ni][e] *= g.alpha;
+  }
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -151,12 +179,7 @@ __global__ void __launch_bounds__(THREADS) dgemm_kernel(GemmArgs g) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         int64_t gi = m0 + wm * 32 + mi * 8 + row, gj = n0 + wn * 32 + ni * 8 + col + e;
-        if (gi < g.m && gj < g.n) {
-          double* p = C + gi + gj * g.ldc;
-          double v = g.alpha * acc[mi][ni][e];
-          if (g.beta != 0.0) v += g.beta * *p;
-          *p = v;
-        }
+        if (gi < g.m && gj < g.n) C[gi + gj * g.ldc] = acc[mi][ni][e];
       }
 }
 

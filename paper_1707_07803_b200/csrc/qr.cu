@@ -153,13 +153,14 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(PanelArgs p) {
         s_w[col] = tot * tau;
       }
       __syncthreads();
-      for (int idx = t; idx < nr * ncols; idx += QR_THREADS) {
-        int r = idx % nr, col = idx / nr;
-        int64_t gr = r0 + r;
-        if (gr >= jj) {
-          double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
-          chunk[r + (jj + 1 + col) * ld] -= v * s_w[col];
-        }
+      // rank-1 update of the remaining panel columns (no integer division:
+      // each thread keeps its rows and walks the columns)
+      for (int r = t; r < nr; r += QR_THREADS) {
+        const int64_t gr = r0 + r;
+        if (gr < jj) continue;
+        const double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
+        double* rowp = chunk + r + (jj + 1) * ld;
+        for (int col = 0; col < ncols; ++col) rowp[col * ld] -= v * s_w[col];
       }
     }
     // diagonal of R
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
   __shared__ double s_tau[QR_NB];
   __shared__ double red[QR_THREADS / 32];
   __shared__ double s_scal, s_tauj, s_beta;
+  __shared__ double s_red[16 * QR_NB];
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks(), c = (int)cluster.block_rank();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -256,10 +258,11 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
       s_part = tot;
     }
     cluster.sync();
-    if (t == 0) {
-      double sig = 0.0;
-      for (int i = 0; i < CS; ++i) sig += *cluster.map_shared_rank(&s_part, i);
+    if (warp == 0) {
+      // all ranks' partials fetched concurrently over DSMEM, fixed xor-tree sum
+      double sig = lane < CS ? *cluster.map_shared_rank(&s_part, lane) : 0.0;
       const double al = *cluster.map_shared_rank(&s_alpha, (int)(jj / p.rpc));
+      sig = warp_sum(sig);
       double tau = 0.0, beta = al, scal = 0.0;
       if (sig != 0.0) {
         double nrm = sqrt(fma(al, al, sig));
@@ -276,34 +279,47 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
       if (r0 + r > jj) chunk[r + jj * ld] *= scal;
     __syncthreads();
     const int ncols = w - jj - 1;
-    for (int col = warp; col < ncols; col += QR_THREADS / 32) {
-      double acc = 0.0;
+    // partial w = v^T A_panel: each warp owns 4 columns (4 independent chains)
+    for (int col0 = warp * 4; col0 < ncols; col0 += QR_THREADS / 8) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
       for (int r = lane; r < nr; r += 32) {
-        int64_t gr = r0 + r;
+        const int64_t gr = r0 + r;
         if (gr >= jj) {
-          double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
-          acc = fma(v, chunk[r + (jj + 1 + col) * ld], acc);
+          const double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (col0 + u < ncols) acc[u] = fma(v, chunk[r + (jj + 1 + col0 + u) * ld], acc[u]);
         }
       }
-      acc = warp_sum(acc);
-      if (lane == 0) s_wpart[col] = acc;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double sum = warp_sum(acc[u]);
+        if (lane == 0 && col0 + u < ncols) s_wpart[col0 + u] = sum;
+      }
     }
     cluster.sync();
     if (ncols > 0) {
       const double tau = s_tauj;
-      for (int col = t; col < ncols; col += QR_THREADS) {
-        double tot = 0.0;
-        for (int i = 0; i < CS; ++i) tot += cluster.map_shared_rank(s_wpart, i)[col];
-        s_w[col] = tot * tau;
+      // gather every rank's partials concurrently, then sum in rank order
+      for (int idx = t; idx < CS * ncols; idx += QR_THREADS) {
+        const int rk = idx / ncols, col = idx % ncols;
+        s_red[rk * QR_NB + col] = cluster.map_shared_rank(s_wpart, rk)[col];
       }
       __syncthreads();
-      for (int idx = t; idx < nr * ncols; idx += QR_THREADS) {
-        int r = idx % nr, col = idx / nr;
-        int64_t gr = r0 + r;
-        if (gr >= jj) {
-          double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
-          chunk[r + (jj + 1 + col) * ld] -= v * s_w[col];
-        }
+      if (t < ncols) {
+        double tot = 0.0;
+        for (int i = 0; i < CS; ++i) tot += s_red[i * QR_NB + t];
+        s_w[t] = tot * tau;
+      }
+      __syncthreads();
+      // rank-1 update of the remaining panel columns (no integer division:
+      // each thread keeps its rows and walks the columns)
+      for (int r = t; r < nr; r += QR_THREADS) {
+        const int64_t gr = r0 + r;
+        if (gr < jj) continue;
+        const double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
+        double* rowp = chunk + r + (jj + 1) * ld;
+        for (int col = 0; col < ncols; ++col) rowp[col * ld] -= v * s_w[col];
       }
     }
     for (int r = t; r < nr; r += QR_THREADS)

@@ -4,18 +4,21 @@
 //
 // Algorithm: QR preconditioning (Householder QR of the tall orientation,
 // qr.cu) followed by one-sided block Jacobi (Hestenes) on the k x k
-// triangular factor X (zero-padded to kp x kp, kp a multiple of 32).
-// Columns are grouped in blocks of JB = 16; a sweep is the nb-1 rounds of a
+// triangular factor X (zero-padded to kp x kp, kp a multiple of 64).
+// Columns are grouped in blocks of JB = 32; a sweep is the nb-1 rounds of a
 // round-robin tournament over the nb blocks.  Each round is three kernels:
-//   gram  : (pair, row split) CTAs stream their rows of the pair's 32
+//   gram  : (pair, row split) CTAs stream their rows of the pair's 64
 //           columns through shared memory (cp.async double buffering) and
-//           form a partial 32 x 32 Gram matrix on the DMMA pipe;
+//           form a partial 64 x 64 Gram matrix on the DMMA pipe;
 //   eig   : one CTA per pair sums the partials in a fixed order, tests
-//           convergence, diagonalises the Gram matrix with cyclic two-sided
-//           Jacobi in shared memory and re-orthogonalises the accumulated
-//           rotation J (one Newton-Schulz step);
+//           convergence, runs one cyclic two-sided Jacobi sweep on the Gram
+//           matrix in shared memory (FP32-seeded, FP64-renormalised
+//           rotations) and re-orthogonalises the accumulated rotation J with
+//           two Newton-Schulz steps on the DMMA pipe;
 //   apply : (pair, row split, X|V) CTAs stream rows again and multiply by J
 //           on the DMMA pipe, in place.
+// 64-column pairs halve the rounds per sweep (and so the HBM traffic per
+// sweep) relative to 32-column pairs, at the same FLOPs.
 // Iteration stops after a sweep in which no pair needed rotating
 // (|x_p.x_q| <= tol ||x_p|| ||x_q|| for every column pair), which gives
 // singular values to O(eps ||M||) like dgesdd.  Singular values are the
@@ -31,11 +34,13 @@ namespace mpob {
 
 namespace {
 
-constexpr int JB = 16;        // columns per Jacobi block
-constexpr int P2 = 2 * JB;    // columns per pair
-constexpr int CH = 64;        // rows per streamed chunk
+constexpr int JB = 32;        // columns per Jacobi block
+constexpr int P2 = 2 * JB;    // columns per pair (64)
+constexpr int NPR = P2 / 2;   // rotations per inner round (32)
+constexpr int CH = 32;        // rows per streamed chunk
 constexpr int LDR = CH + 4;   // chunk column stride (doubles): conflict-free DMMA fragments
-constexpr int GLD = P2 + 1;
+constexpr int GLD = P2 + 1;   // Gram / J row stride in the eig kernel
+constexpr int JLD = P2 + 4;   // J row stride in the apply kernel (conflict-free B fragments)
 constexpr int JT = 256;
 constexpr int NSEG = P2 * CH / 2;  // 16-byte segments per chunk
 
@@ -69,7 +74,7 @@ __device__ __forceinline__ int64_t gcol(int c, int bx, int by) {
   return c < JB ? (int64_t)bx * JB + c : (int64_t)by * JB + (c - JB);
 }
 
-// issue the cp.async loads of rows [r0, r0 + CH) of the pair's 32 columns
+// issue the cp.async loads of rows [r0, r0 + CH) of the pair's 64 columns
 __device__ __forceinline__ void load_chunk(double* buf, const double* M, int64_t ld,
                                            int64_t r0, int64_t rend, int bx, int by) {
   for (int s = threadIdx.x; s < NSEG; s += JT) {
@@ -93,9 +98,8 @@ struct JacArgs {
   int* skip;       // npairs
   int* flag;       // any rotation in this sweep
   double tol;
-  int inner;       // max inner (32 x 32 Gram) Jacobi sweeps per outer round
+  int inner;       // inner (64 x 64 Gram) Jacobi sweeps per outer round
   int* skiplog;    // profiling only: per (round, pair) skip flags, or null
-  long long* dbg;  // MPO_B200_EIGDBG: clock64 phase counters of pair 0, or null
 };
 
 __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
@@ -104,9 +108,10 @@ __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
   int bx, by;
   pair_of_round(a.nb, a.round, pair, bx, by);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
   const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  double acc[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int nch = (int)cdiv_dev(re - rb, CH);
   if (nch > 0) load_chunk(buf[0], a.X, a.ld, rb, re, bx, by);
   cp_async_commit();
@@ -116,30 +121,49 @@ __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
     cp_async_wait<1>();
     __syncthreads();
     const double* b = buf[i & 1];
-    const double* pa = b + (ti * 8 + (lane >> 2)) * LDR + (lane & 3);
-    const double* pb0 = b + (tj0 * 8 + (lane >> 2)) * LDR + (lane & 3);
-    const double* pb1 = pb0 + 8 * LDR;
+    const double* pa = b + (warp * 8 + (lane >> 2)) * LDR + (lane & 3);
+    const double* pb = b + (lane >> 2) * LDR + (lane & 3);
 #pragma unroll
     for (int k0 = 0; k0 < CH; k0 += 4) {
       const double av = pa[k0];
-      dmma(acc[0], av, pb0[k0]);
-      dmma(acc[1], av, pb1[k0]);
+#pragma unroll
+      for (int tj = 0; tj < 8; ++tj) dmma(acc[tj], av, pb[tj * 8 * LDR + k0]);
     }
     __syncthreads();
   }
   double* G = a.gpart + ((int64_t)pair * a.splits + split) * (P2 * P2);
-  const int gi = ti * 8 + (lane >> 2);
+  const int gi = warp * 8 + (lane >> 2);
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int tj = 0; tj < 8; ++tj)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) G[gi * P2 + (tj0 + u) * 8 + 2 * (lane & 3) + e] = acc[u][e];
+    for (int e = 0; e < 2; ++e) G[gi * P2 + tj * 8 + 2 * (lane & 3) + e] = acc[tj][e];
+}
+
+// 64 x 64 x 64 product on the DMMA pipe, warp w owns output row tile w:
+// out[i][j] = sum_k A(i,k) B(k,j) with A(i,k) = transA ? S[k][i] : S[i][k]
+template <bool TRANS_A>
+__device__ __forceinline__ void mm64(const double* S, const double* B, double (&acc)[8][2],
+                                     int warp, int lane) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < P2; k0 += 4) {
+    const int kk = k0 + (lane & 3), ii = warp * 8 + (lane >> 2);
+    const double av = TRANS_A ? S[kk * GLD + ii] : S[ii * GLD + kk];
+#pragma unroll
+    for (int tj = 0; tj < 8; ++tj) dmma(acc[tj], av, B[kk * GLD + tj * 8 + (lane >> 2)]);
+  }
 }
 
 __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
-  __shared__ double G[P2 * GLD];
-  __shared__ double J[P2 * GLD];
+  extern __shared__ double dsm[];
+  double* G = dsm;              // P2 x GLD
+  double* J = dsm + P2 * GLD;   // P2 x GLD
+  __shared__ unsigned char s_pq[P2 - 1][NPR][2];
+  __shared__ double rc[NPR], rs[NPR], rdp[NPR], rdq[NPR];
+  __shared__ int rflag[NPR];
   __shared__ int s_skip;
-  const int t = threadIdx.x, pair = blockIdx.x;
+  const int t = threadIdx.x, pair = blockIdx.x, lane = t & 31, warp = t >> 5;
   {
     // sum the row-split partial Grams in split order (loads issued first)
     constexpr int PER = P2 * P2 / JT;
@@ -147,21 +171,13 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
     double s[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) s[e] = 0.0;
-    int sp = 0;
-    for (; sp + 4 <= a.splits; sp += 4) {
-      double v[4][PER];
+    for (int sp = 0; sp < a.splits; ++sp) {
+      double v[PER];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int e = 0; e < PER; ++e) v[e] = gp[(int64_t)sp * P2 * P2 + e * JT];
 #pragma unroll
-        for (int e = 0; e < PER; ++e) v[q][e] = gp[(int64_t)(sp + q) * P2 * P2 + e * JT];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int e = 0; e < PER; ++e) s[e] += v[q][e];
+      for (int e = 0; e < PER; ++e) s[e] += v[e];
     }
-    for (; sp < a.splits; ++sp)
-#pragma unroll
-      for (int e = 0; e < PER; ++e) s[e] += gp[(int64_t)sp * P2 * P2 + e * JT];
 #pragma unroll
     for (int e = 0; e < PER; ++e) {
       const int idx = t + e * JT;
@@ -177,13 +193,17 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
     if (i > j) G[i * GLD + j] = G[j * GLD + i];
   }
   __syncthreads();
-  for (int idx = t; idx < P2 * P2; idx += JT) {
-    int i = idx / P2, j = idx % P2;
-    if (i < j) {
-      // sqrt before multiplying: G_ii * G_jj underflows for graded columns
-      double d = sqrt(G[i * GLD + i]) * sqrt(G[j * GLD + j]);
-      if (d > 0.0 && fabs(G[i * GLD + j]) > a.tol * d) s_skip = 0;
+  {
+    bool rot = false;
+    for (int idx = t; idx < P2 * P2; idx += JT) {
+      int i = idx / P2, j = idx % P2;
+      if (i < j) {
+        // sqrt before multiplying: G_ii * G_jj underflows for graded columns
+        double d = sqrt(G[i * GLD + i]) * sqrt(G[j * GLD + j]);
+        if (d > 0.0 && fabs(G[i * GLD + j]) > a.tol * d) rot = true;
+      }
     }
+    if (__syncthreads_or(rot)) s_skip = 0;
   }
   __syncthreads();
   if (t == 0) {
@@ -193,35 +213,28 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
   if (s_skip) return;
   if (t == 0) *a.flag = 1;
 
-  // cyclic two-sided Jacobi on G (parallel circle ordering), three short
-  // phases per round: 16 lanes compute the round's 16 rotations, then all
-  // threads update the rotated columns of G and J, then the rotated rows of
-  // G (folding in the exact 2x2 results).  Rotation parameters are seeded in
-  // FP32 (MUFU rsqrt / rcp, scale-free operands) and renormalised in FP64
-  // so that c^2 + s^2 = 1 to FP64 rounding; the angle is thereby accurate to
-  // ~1e-7 relative, which only affects how much of |gpq| one rotation
-  // removes, never the orthogonality of J.  The FP64 sweep test and the
-  // fresh FP64 Gram of every outer round decide convergence.
-  __shared__ unsigned char s_pq[P2 - 1][P2 / 2][2];
-  __shared__ double rc[P2 / 2], rs[P2 / 2], rdp[P2 / 2], rdq[P2 / 2];
-  __shared__ int rflag[P2 / 2];
-  for (int idx = t; idx < (P2 - 1) * (P2 / 2); idx += JT) {
-    int r = idx / (P2 / 2), i = idx % (P2 / 2), p, q;
+  // cyclic two-sided Jacobi on G (parallel circle ordering), two phases per
+  // round: warp 0 computes the round's 32 rotations, then every thread owns
+  // 2x2 blocks G[{p_u,q_u},{p_v,q_v}] and forms R_u^T B R_v in registers
+  // (no intra-phase dependencies) and rotates J's columns.  Rotation
+  // parameters are seeded in FP32 (MUFU rsqrt / reciprocal on scale-free
+  // operands) and renormalised in FP64 so c^2 + s^2 = 1 to FP64 rounding;
+  // the angle is accurate to ~1e-7 relative, which only affects how much of
+  // |gpq| one rotation removes, never the orthogonality of J.  Fresh FP64
+  // Grams of the outer rounds decide convergence.
+  for (int idx = t; idx < (P2 - 1) * NPR; idx += JT) {
+    int r = idx / NPR, i = idx % NPR, p, q;
     pair_of_round(P2, r, i, p, q);
     s_pq[r][i][0] = (unsigned char)min(p, q);
     s_pq[r][i][1] = (unsigned char)max(p, q);
   }
   __syncthreads();
-  long long c_rot = 0, c_col = 0, c_row = 0, c0 = clock64();
   for (int sweep = 0; sweep < a.inner; ++sweep) {
     int any = 0;
     for (int r = 0; r < P2 - 1; ++r) {
-      long long cr = clock64();
-      if (t < P2 / 2) {
+      if (t < NPR) {
         const int p = s_pq[r][t][0], q = s_pq[r][t][1];
         const double gpp = G[p * GLD + p], gqq = G[q * GLD + q], gpq = G[p * GLD + q];
-        // |gpq| > tol sqrt(gpp gqq) without FP64 rsqrt on the critical path;
-        // the product form is exact unless gpp*gqq underflows (graded columns)
         const double pq = gpp * gqq;
         const bool rot = gpp > 0.0 && gqq > 0.0 &&
                          (pq > 1e-280 ? gpq * gpq > a.tol * a.tol * pq
@@ -239,7 +252,7 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
             df = (float)(fabs(d) * sc);
             gf = (float)(g2 * sc);
           }
-          // MUFU approximations only (rsqrt, reciprocal): ~1e-7 relative
+          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (gqq - gpp) / (2 gpq)
           const float r2 = fmaf(df, df, gf * gf);
           const float tf = __fdividef(gf, df + r2 * rsqrtf(r2));
           const float cf = rsqrtf(fmaf(tf, tf, 1.0f));
@@ -251,105 +264,75 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
           s *= f;
         }
         rc[t] = c; rs[t] = s; rflag[t] = rot;
-        // diagonal after the rotation (same c, s as the G update below)
         rdp[t] = fma(c * c, gpp, fma(-2.0 * c * s, gpq, s * s * gqq));
         rdq[t] = fma(s * s, gpp, fma(2.0 * c * s, gpq, c * c * gqq));
         any |= rot;
       }
       __syncthreads();
-      long long cc1 = clock64();
-      c_rot += cc1 - cr;
-      // one phase: thread (u, v) owns the 2x2 block G[{p_u,q_u}, {p_v,q_v}]
-      // and forms R_u^T B R_v in registers (no intra-phase dependencies);
-      // the same threads rotate columns p_v, q_v of J (two rows each)
-      {
-        const int u = t / (P2 / 2), v = t % (P2 / 2);
+#pragma unroll
+      for (int h = 0; h < NPR * NPR / JT; ++h) {
+        const int idx = t + h * JT, u = idx / NPR, v = idx % NPR;
+        if (!(rflag[u] | rflag[v])) continue;
         const int pu = s_pq[r][u][0], qu = s_pq[r][u][1];
+        if (u == v) {
+          G[pu * GLD + pu] = rdp[u];
+          G[qu * GLD + qu] = rdq[u];
+          G[pu * GLD + qu] = 0.0;
+          G[qu * GLD + pu] = 0.0;
+          continue;
+        }
         const int pv = s_pq[r][v][0], qv = s_pq[r][v][1];
         const double cu = rc[u], su = rs[u], cv = rc[v], sv = rs[v];
-        if (u == v) {
-          if (rflag[u]) {
-            G[pu * GLD + pu] = rdp[u];
-            G[qu * GLD + qu] = rdq[u];
-            G[pu * GLD + qu] = 0.0;
-            G[qu * GLD + pu] = 0.0;
-          }
-        } else if (rflag[u] | rflag[v]) {
-          const double b00 = G[pu * GLD + pv], b01 = G[pu * GLD + qv];
-          const double b10 = G[qu * GLD + pv], b11 = G[qu * GLD + qv];
-          // B R_v (columns), then R_u^T (rows)
-          const double x00 = cv * b00 - sv * b01, x01 = sv * b00 + cv * b01;
-          const double x10 = cv * b10 - sv * b11, x11 = sv * b10 + cv * b11;
-          G[pu * GLD + pv] = cu * x00 - su * x10;
-          G[pu * GLD + qv] = cu * x01 - su * x11;
-          G[qu * GLD + pv] = su * x00 + cu * x10;
-          G[qu * GLD + qv] = su * x01 + cu * x11;
-        }
+        const double b00 = G[pu * GLD + pv], b01 = G[pu * GLD + qv];
+        const double b10 = G[qu * GLD + pv], b11 = G[qu * GLD + qv];
+        const double x00 = cv * b00 - sv * b01, x01 = sv * b00 + cv * b01;
+        const double x10 = cv * b10 - sv * b11, x11 = sv * b10 + cv * b11;
+        G[pu * GLD + pv] = cu * x00 - su * x10;
+        G[pu * GLD + qv] = cu * x01 - su * x11;
+        G[qu * GLD + pv] = su * x00 + cu * x10;
+        G[qu * GLD + qv] = su * x01 + cu * x11;
+      }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int idx = t + h * JT, w = idx / P2, row = idx % P2;
-          if (rflag[w]) {
-            const int p = s_pq[r][w][0], q = s_pq[r][w][1];
-            const double c = rc[w], s = rs[w];
-            const double jp = J[row * GLD + p], jq = J[row * GLD + q];
-            J[row * GLD + p] = c * jp - s * jq;
-            J[row * GLD + q] = s * jp + c * jq;
-          }
-        }
+      for (int h = 0; h < P2 * NPR / JT; ++h) {
+        const int idx = t + h * JT, w = idx / P2, row = idx % P2;
+        if (!rflag[w]) continue;
+        const int p = s_pq[r][w][0], q = s_pq[r][w][1];
+        const double c = rc[w], s = rs[w];
+        const double jp = J[row * GLD + p], jq = J[row * GLD + q];
+        J[row * GLD + p] = c * jp - s * jq;
+        J[row * GLD + q] = s * jp + c * jq;
       }
       __syncthreads();
-      c_col += clock64() - cc1;
     }
     if (!__syncthreads_or(any)) break;
   }
-  if (a.dbg && pair == 0 && t == 0) {
-    a.dbg[0] = c_rot; a.dbg[1] = c_col; a.dbg[2] = c_row; a.dbg[3] = clock64() - c0;
-  }
   // re-orthogonalise J: two Newton-Schulz steps J <- J - J (J^T J - I) / 2
-  // (each squares the orthogonality defect of the accumulated rotations);
-  // the 32 x 32 x 32 products run on the DMMA pipe, two 8x8 tiles per warp
+  // (each squares the orthogonality defect of the accumulated rotations)
   double* E = G;
-  const int lane = t & 31, warp = t >> 5;
-  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
   for (int it = 0; it < 2; ++it) {
     __syncthreads();
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-    for (int k0 = 0; k0 < P2; k0 += 4) {
-      const int kk = k0 + (lane & 3);
-      const double av = J[kk * GLD + ti * 8 + (lane >> 2)];          // (J^T)[i][k]
-      dmma(acc[0], av, J[kk * GLD + tj0 * 8 + (lane >> 2)]);
-      dmma(acc[1], av, J[kk * GLD + (tj0 + 1) * 8 + (lane >> 2)]);
-    }
+    double acc[8][2];
+    mm64<true>(J, J, acc, warp, lane);
+    __syncthreads();
     {
-      const int gi = ti * 8 + (lane >> 2);
+      const int gi = warp * 8 + (lane >> 2);
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int tj = 0; tj < 8; ++tj)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int gj = (tj0 + u) * 8 + 2 * (lane & 3) + e;
-          E[gi * GLD + gj] = acc[u][e] - (gi == gj ? 1.0 : 0.0);
+          const int gj = tj * 8 + 2 * (lane & 3) + e;
+          E[gi * GLD + gj] = acc[tj][e] - (gi == gj ? 1.0 : 0.0);
         }
     }
     __syncthreads();
-    double nv[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-    for (int k0 = 0; k0 < P2; k0 += 4) {
-      const int kk = k0 + (lane & 3);
-      const double av = J[(ti * 8 + (lane >> 2)) * GLD + kk];        // J[i][k]
-      dmma(nv[0], av, E[kk * GLD + tj0 * 8 + (lane >> 2)]);
-      dmma(nv[1], av, E[kk * GLD + (tj0 + 1) * 8 + (lane >> 2)]);
-    }
+    mm64<false>(J, E, acc, warp, lane);
     __syncthreads();
     {
-      const int gi = ti * 8 + (lane >> 2);
+      const int gi = warp * 8 + (lane >> 2);
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+      for (int tj = 0; tj < 8; ++tj)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int gj = (tj0 + u) * 8 + 2 * (lane & 3) + e;
-          J[gi * GLD + gj] -= 0.5 * nv[u][e];
-        }
+        for (int e = 0; e < 2; ++e) J[gi * GLD + tj * 8 + 2 * (lane & 3) + e] -= 0.5 * acc[tj][e];
     }
   }
   __syncthreads();
@@ -358,7 +341,9 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
 }
 
 __global__ void __launch_bounds__(JT) jacobi_apply_kernel(JacArgs a) {
-  __shared__ __align__(16) double buf[2][P2 * LDR];
+  extern __shared__ __align__(16) double asm_[];
+  double* buf0 = asm_;                 // 2 x P2*LDR chunk buffers
+  double* Js = asm_ + 2 * P2 * LDR;    // P2 x JLD
   const int pair = blockIdx.x;
   if (a.skip[pair]) return;
   const int which = blockIdx.y / a.splits, split = blockIdx.y % a.splits;
@@ -366,36 +351,35 @@ __global__ void __launch_bounds__(JT) jacobi_apply_kernel(JacArgs a) {
   int bx, by;
   pair_of_round(a.nb, a.round, pair, bx, by);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double* Jg = a.J + (int64_t)pair * P2 * P2;
-  double bj[8][4];
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) bj[ks][nt] = Jg[(4 * ks + (lane & 3)) * P2 + 8 * nt + (lane >> 2)];
   const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
   const int nch = (int)cdiv_dev(re - rb, CH);
-  if (nch > 0) load_chunk(buf[0], M, a.ld, rb, re, bx, by);
+  if (nch > 0) load_chunk(buf0, M, a.ld, rb, re, bx, by);
   cp_async_commit();
+  const double* Jg = a.J + (int64_t)pair * P2 * P2;
+  for (int idx = threadIdx.x; idx < P2 * P2; idx += JT) Js[(idx / P2) * JLD + idx % P2] = Jg[idx];
+  const int rt = warp & 3, ct0 = (warp >> 2) * 4;
   for (int i = 0; i < nch; ++i) {
-    if (i + 1 < nch) load_chunk(buf[(i + 1) & 1], M, a.ld, rb + (int64_t)(i + 1) * CH, re, bx, by);
+    double* b = buf0 + (i & 1) * P2 * LDR;
+    if (i + 1 < nch)
+      load_chunk(buf0 + ((i + 1) & 1) * P2 * LDR, M, a.ld, rb + (int64_t)(i + 1) * CH, re, bx, by);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    double* b = buf[i & 1];
-    // warp w: rows 8w..8w+7 of the chunk, all 32 columns (in place, warp-local)
-    double av[8];
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) av[ks] = b[(4 * ks + (lane & 3)) * LDR + 8 * warp + (lane >> 2)];
+    // out (CH x 64) = chunk (CH x 64) * J: warp owns row tile rt, col tiles ct0..ct0+3
     double o[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks)
+    for (int ks = 0; ks < P2 / 4; ++ks) {
+      const double av = b[(4 * ks + (lane & 3)) * LDR + rt * 8 + (lane >> 2)];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) dmma(o[nt], av[ks], bj[ks][nt]);
-    __syncwarp();
+      for (int c = 0; c < 4; ++c)
+        dmma(o[c], av, Js[(4 * ks + (lane & 3)) * JLD + (ct0 + c) * 8 + (lane >> 2)]);
+    }
+    __syncthreads();   // every warp has read the chunk
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+    for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) b[(8 * nt + 2 * (lane & 3) + e) * LDR + 8 * warp + (lane >> 2)] = o[nt][e];
+      for (int e = 0; e < 2; ++e)
+        b[((ct0 + c) * 8 + 2 * (lane & 3) + e) * LDR + rt * 8 + (lane >> 2)] = o[c][e];
     __syncthreads();
     const int64_t r0 = rb + (int64_t)i * CH;
     for (int s = threadIdx.x; s < NSEG; s += JT) {
@@ -466,28 +450,6 @@ __global__ void gather_cols_kernel(const double* A, int64_t lda, int64_t rows, c
   }
 }
 
-// dst[perm[i], j] = src[i, j]
-__global__ void scatter_rows_kernel(const double* src, int64_t lds, int64_t rows, int64_t cols,
-                                    const int* perm, double* dst, int64_t ldd) {
-  const int64_t total = rows * cols;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = idx % rows, j = idx / rows;
-    dst[(int64_t)perm[i] + j * ldd] = src[i + j * lds];
-  }
-}
-
-// dst[i, perm[j]] = src[i, j]
-__global__ void scatter_cols_kernel(const double* src, int64_t lds, int64_t rows, int64_t cols,
-                                    const int* perm, double* dst, int64_t ldd) {
-  const int64_t total = rows * cols;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = idx % rows, j = idx / rows;
-    dst[i + (int64_t)perm[j] * ldd] = src[i + j * lds];
-  }
-}
-
 // X (kp x kp, zero padded) = R (upper, k x k) or R^T
 __global__ void tri_transpose_kernel(const double* R, int64_t ldr, int64_t k, int64_t kp,
                                      double* X, int upper) {
@@ -508,6 +470,19 @@ inline int gridn(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 148 * 16));
 }
 
+constexpr size_t EIG_SMEM = sizeof(double) * 2 * P2 * GLD;
+constexpr size_t APPLY_SMEM = sizeof(double) * (2 * P2 * LDR + P2 * JLD);
+
+void set_smem_attrs() {
+  static bool done = false;
+  if (done) return;
+  CK(cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)EIG_SMEM));
+  CK(cudaFuncSetAttribute(jacobi_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)APPLY_SMEM));
+  done = true;
+}
+
 }  // namespace
 
 KernelProfile g_prof;
@@ -515,6 +490,7 @@ KernelProfile g_prof;
 // One-sided block Jacobi on the kp x kp matrix X (in place; columns >= k
 // and rows >= k are zero).  V (kp x kp) accumulates the rotations.
 static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, double* V) {
+  set_smem_attrs();
   set_identity(st, kp, kp, V, kp);
   const int nb = (int)(kp / JB), npairs = nb / 2;
   const double eps = 2.220446049250313e-16;
@@ -524,16 +500,10 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   splits = (int)cdiv(kp, rps);
   DBuf<double> gpart((size_t)npairs * splits * P2 * P2, st), J((size_t)npairs * P2 * P2, st);
   DBuf<int> skip(npairs, st), flag(1, st);
-  static const int inner = std::getenv("MPO_B200_INNER") ? std::atoi(std::getenv("MPO_B200_INNER")) : 1;
+  static const int inner =
+      std::getenv("MPO_B200_INNER") ? std::atoi(std::getenv("MPO_B200_INNER")) : 1;
   JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), J.get(), skip.get(), flag.get(), tol,
-            inner, nullptr, nullptr};
-  static const bool eigdbg = std::getenv("MPO_B200_EIGDBG") != nullptr;
-  DBuf<long long> dbg;
-  if (eigdbg) {
-    dbg.alloc(4, st);
-    CK(cudaMemsetAsync(dbg.get(), 0, 4 * sizeof(long long), st));
-    a.dbg = dbg.get();
-  }
+            inner, nullptr};
   // profiling (bench.py roofline): CUDA events around every round kernel
   const bool prof = g_prof.on;
   DBuf<int> skiplog;
@@ -553,10 +523,10 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
       jacobi_gram_kernel<<<dim3(npairs, splits), JT, 0, st>>>(a);
       CK_LAUNCH();
       if (prof) CK(cudaEventRecord(ev[4 * r + 1], st));
-      jacobi_eig_kernel<<<npairs, JT, 0, st>>>(a);
+      jacobi_eig_kernel<<<npairs, JT, EIG_SMEM, st>>>(a);
       CK_LAUNCH();
       if (prof) CK(cudaEventRecord(ev[4 * r + 2], st));
-      jacobi_apply_kernel<<<dim3(npairs, 2 * splits), JT, 0, st>>>(a);
+      jacobi_apply_kernel<<<dim3(npairs, 2 * splits), JT, APPLY_SMEM, st>>>(a);
       CK_LAUNCH();
       if (prof) CK(cudaEventRecord(ev[4 * r + 3], st));
     }
@@ -573,19 +543,13 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
         CK(cudaEventElapsedTime(&t2, ev[4 * r + 2], ev[4 * r + 3]));
         int active = 0;
         for (int p = 0; p < npairs; ++p) active += sk[(size_t)r * npairs + p] == 0;
-        const double unit = 2.0 * (double)kp * P2 * P2;  // one 32-column block of one matrix
+        const double unit = 2.0 * (double)kp * P2 * P2;  // one pair block of one matrix
         g_prof.add(0, t0, unit * npairs);
         g_prof.add(1, t1, 0.0);
         g_prof.add(2, t2, 2.0 * unit * active);
       }
     }
     ++sweeps;
-    if (eigdbg) {
-      long long hd[4];
-      CK(cudaMemcpy(hd, dbg.get(), sizeof(hd), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[mpo_b200] eig k=%lld sweep %d clocks: rot %lld col %lld row %lld total %lld\n",
-              (long long)k, sweeps, hd[0], hd[1], hd[2], hd[3]);
-    }
     if (!h_flag) break;
   }
   for (auto& e : ev) cudaEventDestroy(e);
@@ -611,30 +575,6 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
     }
   } else {
     copy_matrix(st, m, n, M, ldm, A.get(), m);
-  }
-  // pre-pivoting: order the tall orientation's columns by decreasing norm
-  // before the QR (a cheap stand-in for QR with column pivoting, which
-  // grades T's diagonal and shortens the Jacobi iteration)
-  static const bool presort = !std::getenv("MPO_B200_NOPRESORT");
-  DBuf<int> cperm;
-  if (presort && k > 1) {
-    int np2c = 1;
-    while (np2c < k) np2c <<= 1;
-    if (np2c <= 8192) {
-      DBuf<double> cn(k, st), A2((size_t)tm * k, st);
-      cperm.alloc(k, st);
-      col_norms_kernel<<<(int)cdiv(k, 8), 256, 0, st>>>(A.get(), tm, tm, k, cn.get());
-      CK_LAUNCH();
-      const size_t sm = (size_t)np2c * (sizeof(double) + sizeof(int));
-      if (sm > 48 * 1024)
-        CK(cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      sort_desc_kernel<<<1, 1024, sm, st>>>(cn.get(), (int)k, np2c, cn.get(), cperm.get());
-      CK_LAUNCH();
-      gather_cols_kernel<<<gridn(tm * k), 256, 0, st>>>(A.get(), tm, tm, cperm.get(), k, A2.get(), tm);
-      CK_LAUNCH();
-      note_launch(3);
-      A = std::move(A2);
-    }
   }
   householder_qr(st, tm, k, A.get(), tm, Q.get(), tm, R.get(), k);
   // X = T^T (wide) or T (tall), zero padded to kp x kp
@@ -676,30 +616,15 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   out.ucarry.alloc((size_t)m * k, st);
   out.vh.alloc((size_t)k * n, st);
   if (wide) {
-    // P^T M = X Q^T, X Vs = Ys:  Ucarry = P Ys (m = k rows),  Vh = (Q Vs)^T
-    if (cperm.size())
-      scatter_rows_kernel<<<gridn(k * k), 256, 0, st>>>(Ys.get(), k, k, k, cperm.get(),
-                                                         out.ucarry.get(), m);
-    else
-      copy_matrix(st, k, k, Ys.get(), k, out.ucarry.get(), m);
+    // M = X Q^T, X Vs = Ys:  Ucarry = Ys (m = k rows),  Vh = Vs^T Q^T = (Q Vs)^T
+    copy_matrix(st, k, k, Ys.get(), k, out.ucarry.get(), m);
     dgemm(st, true, true, k, n, k, 1.0, Vs.get(), k, Q.get(), tm, 0.0, out.vh.get(), k);
   } else {
-    // M P = Q X:  Ucarry = Q Ys,  Vh = Vs^T P^T
+    // M = Q X:  Ucarry = Q Ys,  Vh = Vs^T
     dgemm(st, false, false, m, k, k, 1.0, Q.get(), tm, Ys.get(), k, 0.0, out.ucarry.get(), m);
     int64_t dims[2] = {k, k};
     int pr[2] = {1, 0};
-    if (cperm.size()) {
-      DBuf<double> vt((size_t)k * k, st);
-      permute(st, Vs.get(), vt.get(), 2, dims, pr);
-      scatter_cols_kernel<<<gridn(k * k), 256, 0, st>>>(vt.get(), k, k, k, cperm.get(),
-                                                         out.vh.get(), k);
-    } else {
-      permute(st, Vs.get(), out.vh.get(), 2, dims, pr);
-    }
-  }
-  if (cperm.size()) {
-    CK_LAUNCH();
-    note_launch();
+    permute(st, Vs.get(), out.vh.get(), 2, dims, pr);
   }
 }
 
