@@ -31,6 +31,7 @@ struct PanelArgs {
   int w;           // panel width
   int rpc;         // rows per CTA
   double* V;       // mp x w explicit reflectors (unit diagonal, zeros above)
+  int64_t ldv;
   double* T;       // w x w compact-WY factor (column-major)
   double* tau;     // w
   double* part;    // G partial norms
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(PanelArgs p) {
     double x = chunk[r + col * ld];
     p.A[gr + col * p.lda] = x;
     double v = gr > col ? x : (gr == col ? 1.0 : 0.0);
-    p.V[gr + (int64_t)col * p.mp] = v;
+    p.V[gr + (int64_t)col * p.ldv] = v;
     chunk[r + col * ld] = v;
   }
   __syncthreads();
@@ -216,6 +217,7 @@ struct ClusterPanelArgs {
   int w;
   int rpc;
   double* V;
+  int64_t ldv;
   double* T;
   double* tau;
 };
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
     double x = chunk[r + col * ld];
     p.A[gr + col * p.lda] = x;
     double v = gr > col ? x : (gr == col ? 1.0 : 0.0);
-    p.V[gr + (int64_t)col * p.mp] = v;
+    p.V[gr + (int64_t)col * p.ldv] = v;
     chunk[r + col * ld] = v;
   }
   __syncthreads();
@@ -408,71 +410,116 @@ int max_coresident_panel_ctas(size_t smem) {
 
 }  // namespace
 
+// one panel of width w at A (mp rows, ld lda): reflectors to V (ld ldv),
+// compact-WY factor to T (w x w), tau to tau
+static void factor_panel(cudaStream_t st, double* A, int64_t lda, int64_t mp, int w, double* V,
+                         int64_t ldv, double* T, double* tau, double* part, double* wpart,
+                         double* vtv, double* alpha) {
+  // preferred: one thread-block cluster (<= 16 CTAs, DSMEM reductions)
+  const int64_t crpc = cdiv(std::max<int64_t>(64, cdiv(mp, 16)), 8) * 8;
+  const size_t csmem = (size_t)crpc * w * sizeof(double);
+  if ((int64_t)csmem <= cluster_smem_limit()) {
+    const int CS = (int)cdiv(mp, crpc);
+    ClusterPanelArgs ca{A, lda, mp, w, (int)crpc, V, ldv, T, tau};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS);
+    cfg.blockDim = dim3(QR_THREADS);
+    cfg.dynamicSmemBytes = csmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel, ca));
+  } else {
+    const int gmax = 148;
+    int64_t rpc = std::max<int64_t>(32, cdiv(mp, gmax));
+    size_t smem = (size_t)rpc * w * sizeof(double);
+    if ((int64_t)smem > panel_smem_limit())
+      throw ValueError("QR panel too tall for the cooperative panel kernel");
+    int G = (int)cdiv(mp, rpc);
+    if (G > max_coresident_panel_ctas(smem)) throw CudaError("QR panel grid not co-resident");
+    PanelArgs pa{A, lda, mp, w, (int)rpc, V, ldv, T, tau, part, wpart, vtv, alpha};
+    void* args[] = {&pa};
+    CK(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QR_THREADS), args, smem,
+                                   st));
+  }
+  note_launch();
+}
+
+// Two-level blocked Householder QR: panels of QR_NB = 32 columns are
+// factored inside outer blocks of NBO = 128 columns; the panel's reflectors
+// update only the rest of their outer block, and the trailing matrix is
+// updated once per outer block with K = 128 DMMA GEMMs (compute-bound rather
+// than one rank-32 HBM pass per panel).  The outer block's T is assembled
+// from the panels' T's: T = [[T1, -T1 (V1^T V2) T2], [0, T2]].
 void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda, double* Q,
                     int64_t ldq, double* R, int64_t ldr) {
+  constexpr int NBO = 128;
   const int64_t k = std::min(m, n);
   if (k <= 0) return;
-  const int smax = panel_smem_limit();
-  const int64_t nblk = cdiv(k, QR_NB);
-  DBuf<double> V((size_t)m * k, st);          // panel b's reflectors at column offset j0, ld = mp
-  DBuf<double> T((size_t)nblk * QR_NB * QR_NB, st);
-  DBuf<double> tau(k + QR_NB, st);
+  const int64_t nob = cdiv(k, NBO);
+  // per outer block: V (mp x wo, ld mp, zero above the unit diagonal) and T (wo x wo)
+  std::vector<int64_t> voff(nob), wos(nob);
+  int64_t vtotal = 0;
+  for (int64_t b = 0; b < nob; ++b) {
+    const int64_t j0 = b * NBO;
+    wos[b] = std::min<int64_t>(NBO, k - j0);
+    voff[b] = vtotal;
+    vtotal += (m - j0) * wos[b];
+  }
+  DBuf<double> V((size_t)vtotal, st), T((size_t)nob * NBO * NBO, st), tau(k + QR_NB, st);
+  fill_zero(st, V.get(), vtotal);
+  fill_zero(st, T.get(), nob * NBO * NBO);
   const int gmax = 148;
   DBuf<double> part(gmax, st), wpart((size_t)gmax * QR_NB, st),
       vtv((size_t)gmax * QR_NB * QR_NB, st), alpha(1, st);
+  DBuf<double> Tp((size_t)QR_NB * QR_NB, st), S((size_t)NBO * NBO, st), tmp((size_t)NBO * QR_NB, st);
   DBuf<double> W, W2;
-  std::vector<int64_t> voff(nblk);
-  int64_t off = 0;
-  for (int64_t b = 0; b < nblk; ++b) {
-    const int64_t j0 = b * QR_NB;
-    const int w = (int)std::min<int64_t>(QR_NB, k - j0);
-    const int64_t mp = m - j0;
-    voff[b] = off;
-    // rows per CTA: fill up to 148 CTAs, shared memory bound
-    // preferred: one thread-block cluster (<= 16 CTAs, DSMEM reductions)
-    const int64_t crpc = cdiv(std::max<int64_t>(64, cdiv(mp, 16)), 8) * 8;
-    const size_t csmem = (size_t)crpc * w * sizeof(double);
-    if ((int64_t)csmem <= cluster_smem_limit()) {
-      const int CS = (int)cdiv(mp, crpc);
-      ClusterPanelArgs ca{A + j0 + j0 * lda, lda, mp, w, (int)crpc, V.get() + off,
-                          T.get() + b * QR_NB * QR_NB, tau.get() + j0};
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(CS);
-      cfg.blockDim = dim3(QR_THREADS);
-      cfg.dynamicSmemBytes = csmem;
-      cfg.stream = st;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = CS;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      CK(cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel, ca));
-    } else {
-      int64_t rpc = std::max<int64_t>(32, cdiv(mp, gmax));
-      size_t smem = (size_t)rpc * w * sizeof(double);
-      if ((int64_t)smem > smax) throw ValueError("QR panel too tall for the cooperative panel kernel");
-      int G = (int)cdiv(mp, rpc);
-      if (G > max_coresident_panel_ctas(smem)) throw CudaError("QR panel grid not co-resident");
-      PanelArgs pa{A + j0 + j0 * lda, lda, mp, w, (int)rpc, V.get() + off,
-                   T.get() + b * QR_NB * QR_NB, tau.get() + j0, part.get(), wpart.get(), vtv.get(),
-                   alpha.get()};
-      void* args[] = {&pa};
-      CK(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QR_THREADS), args, smem,
-                                     st));
+  auto ensure = [&](int64_t sz) {
+    if ((int64_t)W.size() < sz) { W.alloc((size_t)sz, st); W2.alloc((size_t)sz, st); }
+  };
+  for (int64_t b = 0; b < nob; ++b) {
+    const int64_t j0 = b * NBO, wo = wos[b], mp = m - j0;
+    double* Vo = V.get() + voff[b];
+    double* To = T.get() + b * NBO * NBO;   // ld wo
+    for (int64_t i0 = 0; i0 < wo; i0 += QR_NB) {
+      const int wi = (int)std::min<int64_t>(QR_NB, wo - i0);
+      const int64_t jj = j0 + i0, mpi = m - jj;
+      factor_panel(st, A + jj + jj * lda, lda, mpi, wi, Vo + i0 + i0 * mp, mp, Tp.get(),
+                   tau.get() + jj, part.get(), wpart.get(), vtv.get(), alpha.get());
+      // place the panel's T on the diagonal of the outer T
+      copy_matrix(st, wi, wi, Tp.get(), wi, To + i0 + i0 * wo, wo);
+      if (i0 > 0) {
+        // To[0:i0, i0:i0+wi] = -To[0:i0, 0:i0] (V[:, 0:i0]^T V[:, i0:i0+wi]) Tp
+        dgemm(st, true, false, i0, wi, mp, 1.0, Vo, mp, Vo + i0 * mp, mp, 0.0, S.get(), i0);
+        dgemm(st, false, false, i0, wi, i0, 1.0, To, wo, S.get(), i0, 0.0, tmp.get(), i0);
+        dgemm(st, false, false, i0, wi, wi, -1.0, tmp.get(), i0, Tp.get(), wi, 0.0,
+              To + i0 * wo, wo);
+      }
+      // update the rest of this outer block with the panel's reflectors
+      const int64_t rem = wo - (i0 + wi);
+      if (rem > 0) {
+        double* Ar = A + jj + (jj + wi) * lda;
+        const double* Vi = Vo + i0 + i0 * mp;
+        ensure(wi * rem);
+        dgemm(st, true, false, wi, rem, mpi, 1.0, Vi, mp, Ar, lda, 0.0, W.get(), wi);
+        dgemm(st, true, false, wi, rem, wi, 1.0, Tp.get(), wi, W.get(), wi, 0.0, W2.get(), wi);
+        dgemm(st, false, false, mpi, rem, wi, -1.0, Vi, mp, W2.get(), wi, 1.0, Ar, lda);
+      }
     }
-    note_launch();
-    off += mp * w;
-    // trailing update of columns j0+w .. n-1:  A -= V T^T (V^T A)
-    const int64_t nt = n - (j0 + w);
+    // trailing update of columns j0+wo .. n-1 with the outer block:
+    // A -= V T^T (V^T A)
+    const int64_t nt = n - (j0 + wo);
     if (nt > 0) {
-      double* At = A + j0 + (j0 + w) * lda;
-      if ((int64_t)W.size() < w * nt) { W.alloc((size_t)w * nt, st); W2.alloc((size_t)w * nt, st); }
-      dgemm(st, true, false, w, nt, mp, 1.0, V.get() + voff[b], mp, At, lda, 0.0, W.get(), w);
-      dgemm(st, true, false, w, nt, w, 1.0, T.get() + b * QR_NB * QR_NB, w, W.get(), w, 0.0,
-            W2.get(), w);
-      dgemm(st, false, false, mp, nt, w, -1.0, V.get() + voff[b], mp, W2.get(), w, 1.0, At, lda);
+      double* At = A + j0 + (j0 + wo) * lda;
+      ensure(wo * nt);
+      dgemm(st, true, false, wo, nt, mp, 1.0, Vo, mp, At, lda, 0.0, W.get(), wo);
+      dgemm(st, true, false, wo, nt, wo, 1.0, To, wo, W.get(), wo, 0.0, W2.get(), wo);
+      dgemm(st, false, false, mp, nt, wo, -1.0, Vo, mp, W2.get(), wo, 1.0, At, lda);
     }
   }
   if (R) {
@@ -482,18 +529,17 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
     note_launch();
   }
   if (!Q) return;
-  // dorgqr: Q = H_1 ... H_k [I; 0], blocks applied last to first
+  // dorgqr: Q = H_1 ... H_k [I; 0], outer blocks applied last to first
   set_identity(st, m, k, Q, ldq);
-  for (int64_t b = nblk - 1; b >= 0; --b) {
-    const int64_t j0 = b * QR_NB;
-    const int w = (int)std::min<int64_t>(QR_NB, k - j0);
-    const int64_t mp = m - j0, nq = k - j0;
+  for (int64_t b = nob - 1; b >= 0; --b) {
+    const int64_t j0 = b * NBO, wo = wos[b], mp = m - j0, nq = k - j0;
+    double* Vo = V.get() + voff[b];
+    double* To = T.get() + b * NBO * NBO;
     double* Qb = Q + j0 + j0 * ldq;
-    if ((int64_t)W.size() < w * nq) { W.alloc((size_t)w * nq, st); W2.alloc((size_t)w * nq, st); }
-    dgemm(st, true, false, w, nq, mp, 1.0, V.get() + voff[b], mp, Qb, ldq, 0.0, W.get(), w);
-    dgemm(st, false, false, w, nq, w, 1.0, T.get() + b * QR_NB * QR_NB, w, W.get(), w, 0.0,
-          W2.get(), w);
-    dgemm(st, false, false, mp, nq, w, -1.0, V.get() + voff[b], mp, W2.get(), w, 1.0, Qb, ldq);
+    ensure(wo * nq);
+    dgemm(st, true, false, wo, nq, mp, 1.0, Vo, mp, Qb, ldq, 0.0, W.get(), wo);
+    dgemm(st, false, false, wo, nq, wo, 1.0, To, wo, W.get(), wo, 0.0, W2.get(), wo);
+    dgemm(st, false, false, mp, nq, wo, -1.0, Vo, mp, W2.get(), wo, 1.0, Qb, ldq);
   }
 }
 

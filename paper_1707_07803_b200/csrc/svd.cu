@@ -42,6 +42,7 @@ constexpr int LDR = CH + 4;   // chunk column stride (doubles): conflict-free DM
 constexpr int GLD = P2 + 1;   // Gram / J row stride in the eig kernel
 constexpr int JLD = P2 + 4;   // J row stride in the apply kernel (conflict-free B fragments)
 constexpr int JT = 256;
+constexpr int ET = 512;       // eig kernel threads
 constexpr int NSEG = P2 * CH / 2;  // 16-byte segments per chunk
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -142,20 +143,20 @@ __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
 // 64 x 64 x 64 product on the DMMA pipe, warp w owns output row tile w:
 // out[i][j] = sum_k A(i,k) B(k,j) with A(i,k) = transA ? S[k][i] : S[i][k]
 template <bool TRANS_A>
-__device__ __forceinline__ void mm64(const double* S, const double* B, double (&acc)[8][2],
-                                     int warp, int lane) {
+__device__ __forceinline__ void mm64(const double* S, const double* B, double (&acc)[4][2],
+                                     int ti, int tj0, int lane) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll 4
   for (int k0 = 0; k0 < P2; k0 += 4) {
-    const int kk = k0 + (lane & 3), ii = warp * 8 + (lane >> 2);
+    const int kk = k0 + (lane & 3), ii = ti * 8 + (lane >> 2);
     const double av = TRANS_A ? S[kk * GLD + ii] : S[ii * GLD + kk];
 #pragma unroll
-    for (int tj = 0; tj < 8; ++tj) dmma(acc[tj], av, B[kk * GLD + tj * 8 + (lane >> 2)]);
+    for (int tj = 0; tj < 4; ++tj) dmma(acc[tj], av, B[kk * GLD + (tj0 + tj) * 8 + (lane >> 2)]);
   }
 }
 
-__global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
+__global__ void __launch_bounds__(ET) jacobi_eig_kernel(JacArgs a) {
   extern __shared__ double dsm[];
   double* G = dsm;              // P2 x GLD
   double* J = dsm + P2 * GLD;   // P2 x GLD
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
   const int t = threadIdx.x, pair = blockIdx.x, lane = t & 31, warp = t >> 5;
   {
     // sum the row-split partial Grams in split order (loads issued first)
-    constexpr int PER = P2 * P2 / JT;
+    constexpr int PER = P2 * P2 / ET;
     const double* gp = a.gpart + (int64_t)pair * a.splits * (P2 * P2) + t;
     double s[PER];
 #pragma unroll
@@ -174,13 +175,13 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
     for (int sp = 0; sp < a.splits; ++sp) {
       double v[PER];
 #pragma unroll
-      for (int e = 0; e < PER; ++e) v[e] = gp[(int64_t)sp * P2 * P2 + e * JT];
+      for (int e = 0; e < PER; ++e) v[e] = gp[(int64_t)sp * P2 * P2 + e * ET];
 #pragma unroll
       for (int e = 0; e < PER; ++e) s[e] += v[e];
     }
 #pragma unroll
     for (int e = 0; e < PER; ++e) {
-      const int idx = t + e * JT;
+      const int idx = t + e * ET;
       G[(idx / P2) * GLD + idx % P2] = s[e];
       J[(idx / P2) * GLD + idx % P2] = (idx / P2 == idx % P2) ? 1.0 : 0.0;
     }
@@ -188,14 +189,14 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
   if (t == 0) s_skip = 1;
   __syncthreads();
   // symmetrise from the upper triangle
-  for (int idx = t; idx < P2 * P2; idx += JT) {
+  for (int idx = t; idx < P2 * P2; idx += ET) {
     int i = idx / P2, j = idx % P2;
     if (i > j) G[i * GLD + j] = G[j * GLD + i];
   }
   __syncthreads();
   {
     bool rot = false;
-    for (int idx = t; idx < P2 * P2; idx += JT) {
+    for (int idx = t; idx < P2 * P2; idx += ET) {
       int i = idx / P2, j = idx % P2;
       if (i < j) {
         // sqrt before multiplying: G_ii * G_jj underflows for graded columns
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
   // the angle is accurate to ~1e-7 relative, which only affects how much of
   // |gpq| one rotation removes, never the orthogonality of J.  Fresh FP64
   // Grams of the outer rounds decide convergence.
-  for (int idx = t; idx < (P2 - 1) * NPR; idx += JT) {
+  for (int idx = t; idx < (P2 - 1) * NPR; idx += ET) {
     int r = idx / NPR, i = idx % NPR, p, q;
     pair_of_round(P2, r, i, p, q);
     s_pq[r][i][0] = (unsigned char)min(p, q);
@@ -270,8 +271,8 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
       }
       __syncthreads();
 #pragma unroll
-      for (int h = 0; h < NPR * NPR / JT; ++h) {
-        const int idx = t + h * JT, u = idx / NPR, v = idx % NPR;
+      for (int h = 0; h < NPR * NPR / ET; ++h) {
+        const int idx = t + h * ET, u = idx / NPR, v = idx % NPR;
         if (!(rflag[u] | rflag[v])) continue;
         const int pu = s_pq[r][u][0], qu = s_pq[r][u][1];
         if (u == v) {
@@ -293,8 +294,8 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
         G[qu * GLD + qv] = su * x01 + cu * x11;
       }
 #pragma unroll
-      for (int h = 0; h < P2 * NPR / JT; ++h) {
-        const int idx = t + h * JT, w = idx / P2, row = idx % P2;
+      for (int h = 0; h < P2 * NPR / ET; ++h) {
+        const int idx = t + h * ET, w = idx / P2, row = idx % P2;
         if (!rflag[w]) continue;
         const int p = s_pq[r][w][0], q = s_pq[r][w][1];
         const double c = rc[w], s = rs[w];
@@ -311,33 +312,34 @@ __global__ void __launch_bounds__(JT) jacobi_eig_kernel(JacArgs a) {
   double* E = G;
   for (int it = 0; it < 2; ++it) {
     __syncthreads();
-    double acc[8][2];
-    mm64<true>(J, J, acc, warp, lane);
+    double acc[4][2];
+    const int ti = warp & 7, tj0 = (warp >> 3) * 4;
+    mm64<true>(J, J, acc, ti, tj0, lane);
     __syncthreads();
     {
-      const int gi = warp * 8 + (lane >> 2);
+      const int gi = ti * 8 + (lane >> 2);
 #pragma unroll
-      for (int tj = 0; tj < 8; ++tj)
+      for (int tj = 0; tj < 4; ++tj)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int gj = tj * 8 + 2 * (lane & 3) + e;
+          const int gj = (tj0 + tj) * 8 + 2 * (lane & 3) + e;
           E[gi * GLD + gj] = acc[tj][e] - (gi == gj ? 1.0 : 0.0);
         }
     }
     __syncthreads();
-    mm64<false>(J, E, acc, warp, lane);
+    mm64<false>(J, E, acc, ti, tj0, lane);
     __syncthreads();
     {
-      const int gi = warp * 8 + (lane >> 2);
+      const int gi = ti * 8 + (lane >> 2);
 #pragma unroll
-      for (int tj = 0; tj < 8; ++tj)
+      for (int tj = 0; tj < 4; ++tj)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) J[gi * GLD + tj * 8 + 2 * (lane & 3) + e] -= 0.5 * acc[tj][e];
+        for (int e = 0; e < 2; ++e) J[gi * GLD + (tj0 + tj) * 8 + 2 * (lane & 3) + e] -= 0.5 * acc[tj][e];
     }
   }
   __syncthreads();
   double* Jout = a.J + (int64_t)pair * P2 * P2;
-  for (int idx = t; idx < P2 * P2; idx += JT) Jout[idx] = J[(idx / P2) * GLD + idx % P2];
+  for (int idx = t; idx < P2 * P2; idx += ET) Jout[idx] = J[(idx / P2) * GLD + idx % P2];
 }
 
 __global__ void __launch_bounds__(JT) jacobi_apply_kernel(JacArgs a) {
@@ -523,7 +525,7 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
       jacobi_gram_kernel<<<dim3(npairs, splits), JT, 0, st>>>(a);
       CK_LAUNCH();
       if (prof) CK(cudaEventRecord(ev[4 * r + 1], st));
-      jacobi_eig_kernel<<<npairs, JT, EIG_SMEM, st>>>(a);
+      jacobi_eig_kernel<<<npairs, ET, EIG_SMEM, st>>>(a);
       CK_LAUNCH();
       if (prof) CK(cudaEventRecord(ev[4 * r + 2], st));
       jacobi_apply_kernel<<<dim3(npairs, 2 * splits), JT, APPLY_SMEM, st>>>(a);
