@@ -72,6 +72,42 @@ __device__ void build_t_factor(const double* S, double* sT, const double* tau_in
   for (int idx = t; idx < w; idx += blockDim.x) tau_out[idx] = tau_in[idx];
 }
 
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 "
+      "{%0, %1}, {%2}, {%3}, {%0, %1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// out[a + b*w] = sum_r V[r][a] V[r][b] for a < b (else 0) over this CTA's nr
+// rows of the explicit reflectors held column-major in smem (ld rows).  On
+// the DMMA pipe: 16 8x8 tiles, two per warp, K = rows in steps of 4.
+__device__ void vtv_partial_dmma(const double* V, int ld, int nr, int w, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  const int ia = ti * 8 + (lane >> 2);
+  for (int k0 = 0; k0 < nr; k0 += 4) {
+    const int kk = k0 + (lane & 3);
+    const bool kin = kk < nr;
+    const double av = (kin && ia < w) ? V[kk + ia * ld] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int jb = (tj0 + u) * 8 + (lane >> 2);
+      const double bv = (kin && jb < w) ? V[kk + jb * ld] : 0.0;
+      dmma884(acc[u], av, bv);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int b = (tj0 + u) * 8 + 2 * (lane & 3) + e;
+      if (ia < w && b < w) out[ia + b * w] = ia < b ? acc[u][e] : 0.0;
+    }
+}
+
 __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(PanelArgs p) {
   extern __shared__ double chunk[];  // rpc x w, column-major: chunk[r + col*ld]
   __shared__ double red[QR_THREADS / 32];
@@ -181,13 +217,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(PanelArgs p) {
     chunk[r + col * ld] = v;
   }
   __syncthreads();
-  for (int idx = t; idx < w * w; idx += QR_THREADS) {
-    int a = idx % w, b = idx / w;
-    double acc = 0.0;
-    if (a < b)
-      for (int r = 0; r < nr; ++r) acc = fma(chunk[r + a * ld], chunk[r + b * ld], acc);
-    p.vtv[(int64_t)c * w * w + idx] = acc;
-  }
+  vtv_partial_dmma(chunk, ld, nr, w, p.vtv + (int64_t)c * w * w);
   __threadfence();
   grid.sync();
   if (c == 0) {
@@ -338,13 +368,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
     chunk[r + col * ld] = v;
   }
   __syncthreads();
-  for (int idx = t; idx < w * w; idx += QR_THREADS) {
-    int a = idx % w, b = idx / w;
-    double acc = 0.0;
-    if (a < b)
-      for (int r = 0; r < nr; ++r) acc = fma(chunk[r + a * ld], chunk[r + b * ld], acc);
-    s_vtv[idx] = acc;
-  }
+  vtv_partial_dmma(chunk, ld, nr, w, s_vtv);
   cluster.sync();
   if (c == 0) {
     // sum the V^T V partials (fixed rank order) in place, then dlarft
