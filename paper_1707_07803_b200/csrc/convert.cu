@@ -172,24 +172,39 @@ __global__ void radix_hist(const uint64_t* __restrict__ key, int64_t n, int shif
   }
 }
 
-__global__ void radix_scatter(const uint64_t* __restrict__ key, const unsigned* __restrict__ pay,
-                              int64_t n, int shift, const int64_t* __restrict__ offs,
-                              int64_t ntiles, uint64_t* __restrict__ key_out,
-                              unsigned* __restrict__ pay_out) {
+// Stable scatter of one 8-bit digit pass.  Keys are ranked inside the tile
+// (warp-private counters, then a digit-major prefix), staged in shared
+// memory in digit order, and written out as contiguous per-digit runs so
+// the global stores coalesce (a direct scatter would touch one 32-byte
+// sector per 8-byte key).
+constexpr size_t SCATTER_SMEM = (size_t)TILE * (sizeof(uint64_t) + sizeof(unsigned));
+
+__global__ void __launch_bounds__(CT) radix_scatter(const uint64_t* __restrict__ key,
+                                                    const unsigned* __restrict__ pay, int64_t n,
+                                                    int shift, const int64_t* __restrict__ offs,
+                                                    int64_t ntiles, uint64_t* __restrict__ key_out,
+                                                    unsigned* __restrict__ pay_out) {
+  extern __shared__ __align__(16) unsigned char ssm[];
+  uint64_t* skey = reinterpret_cast<uint64_t*>(ssm);
+  unsigned* spay = reinterpret_cast<unsigned*>(ssm + (size_t)TILE * sizeof(uint64_t));
   __shared__ unsigned wh[WARPS][RADIX];
+  __shared__ unsigned dstart[RADIX];
   __shared__ int64_t tbase[RADIX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int d = threadIdx.x; d < WARPS * RADIX; d += CT) (&wh[0][0])[d] = 0;
   for (int d = threadIdx.x; d < RADIX; d += CT) tbase[d] = offs[(int64_t)d * ntiles + blockIdx.x];
   __syncthreads();
-  const int64_t wbase = blockIdx.x * (int64_t)TILE + warp * WITEMS;
+  const int64_t tstart = blockIdx.x * (int64_t)TILE;
+  const int tcount = (int)((n - tstart) < TILE ? (n - tstart) : TILE);
+  const int64_t wbase = tstart + warp * WITEMS;
   uint64_t k[ITEMS];
-  unsigned rank[ITEMS];
+  unsigned pv[ITEMS], rank[ITEMS];
 #pragma unroll
   for (int it = 0; it < ITEMS; ++it) {
     int64_t i = wbase + it * 32 + lane;
     bool valid = i < n;
     k[it] = valid ? key[i] : 0;
+    pv[it] = valid ? pay[i] : 0;
     unsigned dig = valid ? (unsigned)((k[it] >> shift) & (RADIX - 1)) : RADIX;
     unsigned peers = __match_any_sync(0xffffffffu, dig);
     int leader = __ffs(peers) - 1;
@@ -200,10 +215,25 @@ __global__ void radix_scatter(const uint64_t* __restrict__ key, const unsigned* 
     __syncwarp();
   }
   __syncthreads();
-  // exclusive prefix over warps per digit
-  for (int d = threadIdx.x; d < RADIX; d += CT) {
+  // per digit: exclusive prefix over warps, and the digit's tile total
+  if (threadIdx.x < RADIX) {
+    const int d = threadIdx.x;
     unsigned acc = 0;
     for (int w = 0; w < WARPS; ++w) { unsigned v = wh[w][d]; wh[w][d] = acc; acc += v; }
+    dstart[d] = acc;
+  }
+  __syncthreads();
+  // exclusive scan of the 256 digit totals (Hillis-Steele, one value/thread)
+  {
+    unsigned v = threadIdx.x < RADIX ? dstart[threadIdx.x] : 0;
+    const unsigned orig = v;
+    for (int o = 1; o < RADIX; o <<= 1) {
+      unsigned add = (threadIdx.x >= o && threadIdx.x < RADIX) ? dstart[threadIdx.x - o] : 0;
+      __syncthreads();
+      if (threadIdx.x < RADIX) { v += add; dstart[threadIdx.x] = v; }
+      __syncthreads();
+    }
+    if (threadIdx.x < RADIX) dstart[threadIdx.x] = v - orig;
   }
   __syncthreads();
 #pragma unroll
@@ -211,10 +241,18 @@ __global__ void radix_scatter(const uint64_t* __restrict__ key, const unsigned* 
     int64_t i = wbase + it * 32 + lane;
     if (i < n) {
       unsigned dig = (unsigned)((k[it] >> shift) & (RADIX - 1));
-      int64_t o = tbase[dig] + wh[warp][dig] + rank[it];
-      key_out[o] = k[it];
-      pay_out[o] = pay[i];
+      unsigned lp = dstart[dig] + wh[warp][dig] + rank[it];
+      skey[lp] = k[it];
+      spay[lp] = pv[it];
     }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < tcount; j += CT) {
+    const uint64_t kk = skey[j];
+    const unsigned dig = (unsigned)((kk >> shift) & (RADIX - 1));
+    const int64_t o = tbase[dig] + (j - (int64_t)dstart[dig]);
+    key_out[o] = kk;
+    pay_out[o] = spay[j];
   }
 }
 
@@ -307,6 +345,12 @@ void radix_sort_pairs(cudaStream_t st, uint64_t* key, unsigned* pay, int64_t n, 
   result_in_tmp = false;
   if (n <= 1 || bits == 0) return;
   const int64_t ntiles = cdiv(n, TILE);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)SCATTER_SMEM));
+    attr = true;
+  }
   DBuf<unsigned> hist((size_t)RADIX * ntiles, st);
   DBuf<int64_t> offs((size_t)RADIX * ntiles, st), total(1, st);
   uint64_t *ks = key, *kd = key_tmp;
@@ -315,7 +359,8 @@ void radix_sort_pairs(cudaStream_t st, uint64_t* key, unsigned* pay, int64_t n, 
     radix_hist<<<(int)ntiles, CT, 0, st>>>(ks, n, shift, hist.get(), ntiles);
     CK_LAUNCH();
     exclusive_scan_u32(st, hist.get(), RADIX * ntiles, offs.get(), total.get());
-    radix_scatter<<<(int)ntiles, CT, 0, st>>>(ks, ps, n, shift, offs.get(), ntiles, kd, pd);
+    radix_scatter<<<(int)ntiles, CT, SCATTER_SMEM, st>>>(ks, ps, n, shift, offs.get(), ntiles, kd,
+                                                          pd);
     CK_LAUNCH();
     note_launch(2);
     std::swap(ks, kd);

@@ -13,7 +13,7 @@ for r in csv.reader(open(sys.argv[1])):
         continue
     name = d["Kernel Name"].split("(")[0].replace("(anonymous namespace)::", "")
     v = float(d["Metric Value"].replace(",", ""))
-    v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(d["Metric Unit"], 1.0)
+    v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6}.get(d["Metric Unit"], 1.0)
     agg[name][0] += 1
     agg[name][1] += v
 tot = sum(t for _, t in agg.values())
