@@ -101,6 +101,7 @@ struct JacArgs {
   double tol;
   int inner;       // inner (64 x 64 Gram) Jacobi sweeps per outer round
   int* skiplog;    // profiling only: per (round, pair) skip flags, or null
+  int which;       // apply: 0 = X, 1 = V
 };
 
 __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
@@ -110,9 +111,20 @@ __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
   pair_of_round(a.nb, a.round, pair, bx, by);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
-  double acc[8][2];
+  // the Gram matrix is symmetric: only the 36 upper-triangle 8x8 tiles
+  // (ti <= tj) are formed, tiles w, w+8, ... per warp (4-5 each)
+  int tiw[5], tjw[5];
+  const int ntw = warp < 4 ? 5 : 4;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int u = 0; u < 5; ++u) {
+    int idx = min(warp + 8 * u, 35), ti = 0;
+    while (idx >= 8 - ti) { idx -= 8 - ti; ++ti; }   // idx -> (ti, tj >= ti), idx < 36
+    tiw[u] = ti;
+    tjw[u] = ti + idx;
+  }
+  double acc[5][2];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int nch = (int)cdiv_dev(re - rb, CH);
   if (nch > 0) load_chunk(buf[0], a.X, a.ld, rb, re, bx, by);
   cp_async_commit();
@@ -121,23 +133,23 @@ __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const double* b = buf[i & 1];
-    const double* pa = b + (warp * 8 + (lane >> 2)) * LDR + (lane & 3);
-    const double* pb = b + (lane >> 2) * LDR + (lane & 3);
+    const double* b = buf[i & 1] + (lane >> 2) * LDR + (lane & 3);
 #pragma unroll
     for (int k0 = 0; k0 < CH; k0 += 4) {
-      const double av = pa[k0];
 #pragma unroll
-      for (int tj = 0; tj < 8; ++tj) dmma(acc[tj], av, pb[tj * 8 * LDR + k0]);
+      for (int u = 0; u < 5; ++u)
+        if (u < ntw) dmma(acc[u], b[tiw[u] * 8 * LDR + k0], b[tjw[u] * 8 * LDR + k0]);
     }
     __syncthreads();
   }
   double* G = a.gpart + ((int64_t)pair * a.splits + split) * (P2 * P2);
-  const int gi = warp * 8 + (lane >> 2);
 #pragma unroll
-  for (int tj = 0; tj < 8; ++tj)
+  for (int u = 0; u < 5; ++u)
+    if (u < ntw) {
+      const int gi = tiw[u] * 8 + (lane >> 2);
 #pragma unroll
-    for (int e = 0; e < 2; ++e) G[gi * P2 + tj * 8 + 2 * (lane & 3) + e] = acc[tj][e];
+      for (int e = 0; e < 2; ++e) G[gi * P2 + tjw[u] * 8 + 2 * (lane & 3) + e] = acc[u][e];
+    }
 }
 
 // 64 x 64 x 64 product on the DMMA pipe, warp w owns output row tile w:
@@ -348,7 +360,7 @@ __global__ void __launch_bounds__(JT) jacobi_apply_kernel(JacArgs a) {
   double* Js = asm_ + 2 * P2 * LDR;    // P2 x JLD
   const int pair = blockIdx.x;
   if (a.skip[pair]) return;
-  const int which = blockIdx.y / a.splits, split = blockIdx.y % a.splits;
+  const int which = a.which, split = blockIdx.y;
   double* M = which == 0 ? a.X : a.V;
   int bx, by;
   pair_of_round(a.nb, a.round, pair, bx, by);
@@ -504,9 +516,18 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   DBuf<int> skip(npairs, st), flag(1, st);
   static const int inner =
       std::getenv("MPO_B200_INNER") ? std::atoi(std::getenv("MPO_B200_INNER")) : 1;
-  JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), J.get(), skip.get(), flag.get(), tol,
-            inner, nullptr};
-  // profiling (bench.py roofline): CUDA events around every round kernel
+  // J and skip flags are double-buffered by round parity: the V updates of
+  // round r run on a second stream, overlapping the gram / eig of round
+  // r+1 (V is never read by the iteration itself), and the eig of round
+  // r+2 waits for them before reusing the buffers.
+  DBuf<double> J2((size_t)npairs * P2 * P2, st);
+  DBuf<int> skip2(npairs, st);
+  double* Jb[2] = {J.get(), J2.get()};
+  int* Sb[2] = {skip.get(), skip2.get()};
+  JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), Jb[0], Sb[0], flag.get(), tol,
+            inner, nullptr, 0};
+  // profiling (bench.py roofline): CUDA events around every round kernel;
+  // the V updates then stay on the main stream so the intervals are exact
   const bool prof = g_prof.on;
   DBuf<int> skiplog;
   std::vector<cudaEvent_t> ev;
@@ -516,23 +537,47 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
     ev.resize(4 * (nb - 1));
     for (auto& e : ev) CK(cudaEventCreate(&e));
   }
+  cudaStream_t sv = st;
+  cudaEvent_t evE[2] = {nullptr, nullptr}, evV[2] = {nullptr, nullptr};
+  const bool overlap = !prof && npairs > 1;
+  if (overlap) {
+    CK(cudaStreamCreateWithFlags(&sv, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&evE[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&evV[i], cudaEventDisableTiming));
+      CK(cudaEventRecord(evV[i], st));
+    }
+    CK(cudaStreamWaitEvent(sv, evV[0], 0));   // V = I is ready
+  }
   int h_flag = 0, sweeps = 0;
+  int64_t rr = 0;   // global round counter (buffer parity across sweeps)
   for (int sweep = 0; sweep < 60; ++sweep) {
     CK(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
-    for (int r = 0; r < nb - 1; ++r) {
+    for (int r = 0; r < nb - 1; ++r, ++rr) {
+      const int par = (int)(rr & 1);
       a.round = r;
+      a.J = Jb[par];
+      a.skip = Sb[par];
       if (prof) CK(cudaEventRecord(ev[4 * r], st));
       jacobi_gram_kernel<<<dim3(npairs, splits), JT, 0, st>>>(a);
       CK_LAUNCH();
       if (prof) CK(cudaEventRecord(ev[4 * r + 1], st));
+      if (overlap) CK(cudaStreamWaitEvent(st, evV[par], 0));
       jacobi_eig_kernel<<<npairs, ET, EIG_SMEM, st>>>(a);
       CK_LAUNCH();
       if (prof) CK(cudaEventRecord(ev[4 * r + 2], st));
-      jacobi_apply_kernel<<<dim3(npairs, 2 * splits), JT, APPLY_SMEM, st>>>(a);
+      if (overlap) CK(cudaEventRecord(evE[par], st));
+      a.which = 0;
+      jacobi_apply_kernel<<<dim3(npairs, splits), JT, APPLY_SMEM, st>>>(a);
       CK_LAUNCH();
+      a.which = 1;
+      if (overlap) CK(cudaStreamWaitEvent(sv, evE[par], 0));
+      jacobi_apply_kernel<<<dim3(npairs, splits), JT, APPLY_SMEM, sv>>>(a);
+      CK_LAUNCH();
+      if (overlap) CK(cudaEventRecord(evV[par], sv));
       if (prof) CK(cudaEventRecord(ev[4 * r + 3], st));
     }
-    note_launch(3 * (nb - 1));
+    note_launch(4 * (nb - 1));
     CK(cudaMemcpyAsync(&h_flag, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (prof) {
@@ -553,6 +598,17 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
     }
     ++sweeps;
     if (!h_flag) break;
+  }
+  if (overlap) {
+    // the main stream continues only after the last V update
+    CK(cudaEventRecord(evV[0], sv));
+    CK(cudaStreamWaitEvent(st, evV[0], 0));
+    CK(cudaStreamSynchronize(sv));
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(evE[i]);
+      cudaEventDestroy(evV[i]);
+    }
+    cudaStreamDestroy(sv);
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return sweeps;
