@@ -539,14 +539,24 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   }
   cudaStream_t sv = st;
   cudaEvent_t evE[2] = {nullptr, nullptr}, evV[2] = {nullptr, nullptr};
-  const bool overlap = !prof && npairs > 1;
+  const bool overlap = !prof && npairs >= 16;   // large problems only
   if (overlap) {
-    CK(cudaStreamCreateWithFlags(&sv, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
-      CK(cudaEventCreateWithFlags(&evE[i], cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&evV[i], cudaEventDisableTiming));
-      CK(cudaEventRecord(evV[i], st));
+    // side stream + events cached per (host thread, main stream)
+    struct Side { cudaStream_t main = nullptr, sv = nullptr; cudaEvent_t e[4]; };
+    thread_local std::vector<Side> sides;
+    Side* sd = nullptr;
+    for (auto& x : sides) if (x.main == st) sd = &x;
+    if (!sd) {
+      Side x;
+      x.main = st;
+      CK(cudaStreamCreateWithFlags(&x.sv, cudaStreamNonBlocking));
+      for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&x.e[i], cudaEventDisableTiming));
+      sides.push_back(x);
+      sd = &sides.back();
     }
+    sv = sd->sv;
+    evE[0] = sd->e[0]; evE[1] = sd->e[1]; evV[0] = sd->e[2]; evV[1] = sd->e[3];
+    for (int i = 0; i < 2; ++i) CK(cudaEventRecord(evV[i], st));
     CK(cudaStreamWaitEvent(sv, evV[0], 0));   // V = I is ready
   }
   int h_flag = 0, sweeps = 0;
@@ -603,12 +613,6 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
     // the main stream continues only after the last V update
     CK(cudaEventRecord(evV[0], sv));
     CK(cudaStreamWaitEvent(st, evV[0], 0));
-    CK(cudaStreamSynchronize(sv));
-    for (int i = 0; i < 2; ++i) {
-      cudaEventDestroy(evE[i]);
-      cudaEventDestroy(evV[i]);
-    }
-    cudaStreamDestroy(sv);
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return sweeps;
