@@ -491,9 +491,9 @@ def gram_first_index(x, y):
         else:
             t = np.tensordot(np.tensordot(cx2, t, axes=(2, 0)), cy2, axes=([1, 2], [1, 2]))
     c0x, c0y = x[0][0], y[0][0]        # (I1, K, R)
-    if t is None:
-        return np.einsum("ikr,ilr->kl", c0x, c0y)
-    return np.einsum("ikr,rs,ils->kl", c0x, t, c0y)
+    if t is not None:
+        c0x = np.tensordot(c0x, t, axes=(2, 0))      # (I1, Kx, Sy)
+    return np.tensordot(c0x, c0y, axes=([0, 2], [0, 2]))
 
 
 def aligned_factor_error(x, y):

@@ -345,12 +345,12 @@ void radix_sort_pairs(cudaStream_t st, uint64_t* key, unsigned* pay, int64_t n, 
   result_in_tmp = false;
   if (n <= 1 || bits == 0) return;
   const int64_t ntiles = cdiv(n, TILE);
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [] {   // thread-safe one-time setup
     CK(cudaFuncSetAttribute(radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)SCATTER_SMEM));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   DBuf<unsigned> hist((size_t)RADIX * ntiles, st);
   DBuf<int64_t> offs((size_t)RADIX * ntiles, st), total(1, st);
   uint64_t *ks = key, *kd = key_tmp;

@@ -393,34 +393,36 @@ __global__ void extract_r_kernel(int64_t k, int64_t n, const double* A, int64_t 
   }
 }
 
+// one-time kernel attribute setup: C++11 magic statics make these
+// thread-safe (the batched path calls in from several host threads)
 int panel_smem_limit() {
-  static int lim = 0;
-  if (!lim) {
-    int dev;
+  static const int lim = [] {
+    int dev, l;
     CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    CK(cudaDeviceGetAttribute(&l, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, qr_panel_kernel));
-    lim -= (int)fa.sharedSizeBytes + 1024;
-    CK(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-  }
+    l -= (int)fa.sharedSizeBytes + 1024;
+    CK(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, l));
+    return l;
+  }();
   return lim;
 }
 
 int cluster_smem_limit() {
-  static int lim = 0;
-  if (!lim) {
-    int dev;
+  static const int lim = [] {
+    int dev, l;
     CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    CK(cudaDeviceGetAttribute(&l, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, qr_panel_cluster_kernel));
-    lim -= (int)fa.sharedSizeBytes + 1024;
+    l -= (int)fa.sharedSizeBytes + 1024;
     CK(cudaFuncSetAttribute(qr_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            lim));
+                            l));
     CK(cudaFuncSetAttribute(qr_panel_cluster_kernel,
                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  }
+    return l;
+  }();
   return lim;
 }
 
@@ -430,6 +432,16 @@ int max_coresident_panel_ctas(size_t smem) {
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, qr_panel_kernel, QR_THREADS, smem));
   return std::max(1, per) * nsm;
+}
+
+// widest panel (<= wmax columns) whose rows fit the panel kernels' shared
+// memory: very tall, narrow matrices (e.g. the 196608 x 48 first core of
+// config 3's B) are factored in narrower panels
+int panel_width(int64_t mp, int wmax) {
+  const int64_t rpc = std::max<int64_t>(32, cdiv(mp, 148));
+  int w = wmax;
+  while (w > 1 && rpc * w * (int64_t)sizeof(double) > panel_smem_limit()) w = (w + 1) / 2;
+  return w;
 }
 
 }  // namespace
@@ -510,9 +522,9 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
     const int64_t j0 = b * NBO, wo = wos[b], mp = m - j0;
     double* Vo = V.get() + voff[b];
     double* To = T.get() + b * NBO * NBO;   // ld wo
-    for (int64_t i0 = 0; i0 < wo; i0 += QR_NB) {
-      const int wi = (int)std::min<int64_t>(QR_NB, wo - i0);
+    for (int64_t i0 = 0, wi = 0; i0 < wo; i0 += wi) {
       const int64_t jj = j0 + i0, mpi = m - jj;
+      wi = std::min<int64_t>(panel_width(mpi, QR_NB), wo - i0);
       factor_panel(st, A + jj + jj * lda, lda, mpi, wi, Vo + i0 + i0 * mp, mp, Tp.get(),
                    tau.get() + jj, part.get(), wpart.get(), vtv.get(), alpha.get());
       // place the panel's T on the diagonal of the outer T

@@ -34,16 +34,23 @@ namespace mpob {
 
 namespace {
 
-constexpr int JB = 32;        // columns per Jacobi block
-constexpr int P2 = 2 * JB;    // columns per pair (64)
-constexpr int NPR = P2 / 2;   // rotations per inner round (32)
+// Block geometry, templated on the column-block width JB (32 for large k:
+// fewer rounds and less HBM traffic per sweep; 16 for small k: the inner
+// 32x32 Jacobi costs a quarter of the 64x64 one, and small problems are
+// bound by that latency).
+template <int JB_>
+struct JK {
+  static constexpr int P2 = 2 * JB_;       // columns per pair (JB_ columns per block)
+  static constexpr int NPR = JB_;          // rotations per inner round
+  static constexpr int NT = P2 / 8;        // 8x8 tiles per dimension
+  static constexpr int GLD = P2 + 1;       // Gram / J row stride in the eig kernel
+  static constexpr int JLD = P2 + 4;       // J row stride in the apply kernel
+  static constexpr int NSEG = P2 * 32 / 2; // 16-byte segments per 32-row chunk
+  static constexpr int ET = P2 == 64 ? 512 : 256;   // eig kernel threads
+};
 constexpr int CH = 32;        // rows per streamed chunk
 constexpr int LDR = CH + 4;   // chunk column stride (doubles): conflict-free DMMA fragments
-constexpr int GLD = P2 + 1;   // Gram / J row stride in the eig kernel
-constexpr int JLD = P2 + 4;   // J row stride in the apply kernel (conflict-free B fragments)
 constexpr int JT = 256;
-constexpr int ET = 512;       // eig kernel threads
-constexpr int NSEG = P2 * CH / 2;  // 16-byte segments per chunk
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile(
@@ -71,18 +78,21 @@ __host__ __device__ __forceinline__ void pair_of_round(int nb, int r, int i, int
   y = slot(nb - 1 - i);
 }
 
+template <int JB>
 __device__ __forceinline__ int64_t gcol(int c, int bx, int by) {
   return c < JB ? (int64_t)bx * JB + c : (int64_t)by * JB + (c - JB);
 }
 
-// issue the cp.async loads of rows [r0, r0 + CH) of the pair's 64 columns
+// issue the cp.async loads of rows [r0, r0 + CH) of the pair's P2 columns
+template <int JB>
 __device__ __forceinline__ void load_chunk(double* buf, const double* M, int64_t ld,
                                            int64_t r0, int64_t rend, int bx, int by) {
-  for (int s = threadIdx.x; s < NSEG; s += JT) {
+  using K = JK<JB>;
+  for (int s = threadIdx.x; s < K::NSEG; s += JT) {
     const int c = s / (CH / 2), rp = s % (CH / 2);
     const int64_t gr = r0 + 2 * rp;
     const bool ok = gr < rend;  // rows come in pairs (kp is even)
-    const double* src = M + (ok ? gr : 0) + gcol(c, bx, by) * ld;
+    const double* src = M + (ok ? gr : 0) + gcol<JB>(c, bx, by) * ld;
     cp_async16(buf + c * LDR + 2 * rp, src, ok ? 16 : 0);
   }
 }
@@ -99,37 +109,42 @@ struct JacArgs {
   int* skip;       // npairs
   int* flag;       // any rotation in this sweep
   double tol;
-  int inner;       // inner (64 x 64 Gram) Jacobi sweeps per outer round
+  int inner;       // inner (P2 x P2 Gram) Jacobi sweeps per outer round
   int* skiplog;    // profiling only: per (round, pair) skip flags, or null
   int which;       // apply: 0 = X, 1 = V
 };
 
+template <int JB>
 __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
+  using K = JK<JB>;
+  constexpr int P2 = K::P2, NT = K::NT, NTT = NT * (NT + 1) / 2, TPW = (NTT + 7) / 8;
   __shared__ __align__(16) double buf[2][P2 * LDR];
   const int pair = blockIdx.x, split = blockIdx.y;
   int bx, by;
   pair_of_round(a.nb, a.round, pair, bx, by);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
-  // the Gram matrix is symmetric: only the 36 upper-triangle 8x8 tiles
-  // (ti <= tj) are formed, tiles w, w+8, ... per warp (4-5 each)
-  int tiw[5], tjw[5];
-  const int ntw = warp < 4 ? 5 : 4;
+  // the Gram matrix is symmetric: only the upper-triangle 8x8 tiles
+  // (ti <= tj) are formed, tiles w, w+8, ... per warp
+  int tiw[TPW], tjw[TPW];
+  int ntw = 0;
 #pragma unroll
-  for (int u = 0; u < 5; ++u) {
-    int idx = min(warp + 8 * u, 35), ti = 0;
-    while (idx >= 8 - ti) { idx -= 8 - ti; ++ti; }   // idx -> (ti, tj >= ti), idx < 36
+  for (int u = 0; u < TPW; ++u) {
+    int idx = min(warp + 8 * u, NTT - 1), ti = 0;
+    while (idx >= NT - ti) { idx -= NT - ti; ++ti; }   // idx -> (ti, tj >= ti)
     tiw[u] = ti;
     tjw[u] = ti + idx;
+    ntw += (warp + 8 * u < NTT);
   }
-  double acc[5][2];
+  double acc[TPW][2];
 #pragma unroll
-  for (int j = 0; j < 5; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int j = 0; j < TPW; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int nch = (int)cdiv_dev(re - rb, CH);
-  if (nch > 0) load_chunk(buf[0], a.X, a.ld, rb, re, bx, by);
+  if (nch > 0) load_chunk<JB>(buf[0], a.X, a.ld, rb, re, bx, by);
   cp_async_commit();
   for (int i = 0; i < nch; ++i) {
-    if (i + 1 < nch) load_chunk(buf[(i + 1) & 1], a.X, a.ld, rb + (int64_t)(i + 1) * CH, re, bx, by);
+    if (i + 1 < nch)
+      load_chunk<JB>(buf[(i + 1) & 1], a.X, a.ld, rb + (int64_t)(i + 1) * CH, re, bx, by);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
@@ -137,14 +152,14 @@ __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
 #pragma unroll
     for (int k0 = 0; k0 < CH; k0 += 4) {
 #pragma unroll
-      for (int u = 0; u < 5; ++u)
+      for (int u = 0; u < TPW; ++u)
         if (u < ntw) dmma(acc[u], b[tiw[u] * 8 * LDR + k0], b[tjw[u] * 8 * LDR + k0]);
     }
     __syncthreads();
   }
   double* G = a.gpart + ((int64_t)pair * a.splits + split) * (P2 * P2);
 #pragma unroll
-  for (int u = 0; u < 5; ++u)
+  for (int u = 0; u < TPW; ++u)
     if (u < ntw) {
       const int gi = tiw[u] * 8 + (lane >> 2);
 #pragma unroll
@@ -152,23 +167,27 @@ __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
     }
 }
 
-// 64 x 64 x 64 product on the DMMA pipe, warp w owns output row tile w:
-// out[i][j] = sum_k A(i,k) B(k,j) with A(i,k) = transA ? S[k][i] : S[i][k]
-template <bool TRANS_A>
-__device__ __forceinline__ void mm64(const double* S, const double* B, double (&acc)[4][2],
-                                     int ti, int tj0, int lane) {
+// P2 x P2 x P2 product on the DMMA pipe over row tile ti, column tiles
+// tj0 .. tj0+C-1: out[i][j] = sum_k A(i,k) B(k,j), A(i,k) = transA ? S[k][i] : S[i][k]
+template <int JB, int C, bool TRANS_A>
+__device__ __forceinline__ void mmP(const double* S, const double* B, double (&acc)[C][2],
+                                    int ti, int tj0, int lane) {
+  using K = JK<JB>;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int j = 0; j < C; ++j) acc[j][0] = acc[j][1] = 0.0;
 #pragma unroll 4
-  for (int k0 = 0; k0 < P2; k0 += 4) {
+  for (int k0 = 0; k0 < K::P2; k0 += 4) {
     const int kk = k0 + (lane & 3), ii = ti * 8 + (lane >> 2);
-    const double av = TRANS_A ? S[kk * GLD + ii] : S[ii * GLD + kk];
+    const double av = TRANS_A ? S[kk * K::GLD + ii] : S[ii * K::GLD + kk];
 #pragma unroll
-    for (int tj = 0; tj < 4; ++tj) dmma(acc[tj], av, B[kk * GLD + (tj0 + tj) * 8 + (lane >> 2)]);
+    for (int tj = 0; tj < C; ++tj) dmma(acc[tj], av, B[kk * K::GLD + (tj0 + tj) * 8 + (lane >> 2)]);
   }
 }
 
-__global__ void __launch_bounds__(ET) jacobi_eig_kernel(JacArgs a) {
+template <int JB>
+__global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
+  using K = JK<JB>;
+  constexpr int P2 = K::P2, NPR = K::NPR, GLD = K::GLD, ET = K::ET;
   extern __shared__ double dsm[];
   double* G = dsm;              // P2 x GLD
   double* J = dsm + P2 * GLD;   // P2 x GLD
@@ -181,20 +200,20 @@ __global__ void __launch_bounds__(ET) jacobi_eig_kernel(JacArgs a) {
     // sum the row-split partial Grams in split order (loads issued first)
     constexpr int PER = P2 * P2 / ET;
     const double* gp = a.gpart + (int64_t)pair * a.splits * (P2 * P2) + t;
-    double s[PER];
+    double sacc[PER];
 #pragma unroll
-    for (int e = 0; e < PER; ++e) s[e] = 0.0;
+    for (int e = 0; e < PER; ++e) sacc[e] = 0.0;
     for (int sp = 0; sp < a.splits; ++sp) {
       double v[PER];
 #pragma unroll
       for (int e = 0; e < PER; ++e) v[e] = gp[(int64_t)sp * P2 * P2 + e * ET];
 #pragma unroll
-      for (int e = 0; e < PER; ++e) s[e] += v[e];
+      for (int e = 0; e < PER; ++e) sacc[e] += v[e];
     }
 #pragma unroll
     for (int e = 0; e < PER; ++e) {
       const int idx = t + e * ET;
-      G[(idx / P2) * GLD + idx % P2] = s[e];
+      G[(idx / P2) * GLD + idx % P2] = sacc[e];
       J[(idx / P2) * GLD + idx % P2] = (idx / P2 == idx % P2) ? 1.0 : 0.0;
     }
   }
@@ -227,7 +246,7 @@ __global__ void __launch_bounds__(ET) jacobi_eig_kernel(JacArgs a) {
   if (t == 0) *a.flag = 1;
 
   // cyclic two-sided Jacobi on G (parallel circle ordering), two phases per
-  // round: warp 0 computes the round's 32 rotations, then every thread owns
+  // round: warp 0 computes the round's rotations, then every thread owns
   // 2x2 blocks G[{p_u,q_u},{p_v,q_v}] and forms R_u^T B R_v in registers
   // (no intra-phase dependencies) and rotates J's columns.  Rotation
   // parameters are seeded in FP32 (MUFU rsqrt / reciprocal on scale-free
@@ -320,18 +339,20 @@ __global__ void __launch_bounds__(ET) jacobi_eig_kernel(JacArgs a) {
     if (!__syncthreads_or(any)) break;
   }
   // re-orthogonalise J: two Newton-Schulz steps J <- J - J (J^T J - I) / 2
-  // (each squares the orthogonality defect of the accumulated rotations)
+  // (each squares the orthogonality defect of the accumulated rotations),
+  // P2^3 products on the DMMA pipe
+  constexpr int NW = ET / 32, TPW = K::NT * K::NT / NW;
   double* E = G;
+  const int ti = warp % K::NT, tj0 = (warp / K::NT) * TPW;
   for (int it = 0; it < 2; ++it) {
     __syncthreads();
-    double acc[4][2];
-    const int ti = warp & 7, tj0 = (warp >> 3) * 4;
-    mm64<true>(J, J, acc, ti, tj0, lane);
+    double acc[TPW][2];
+    mmP<JB, TPW, true>(J, J, acc, ti, tj0, lane);
     __syncthreads();
     {
       const int gi = ti * 8 + (lane >> 2);
 #pragma unroll
-      for (int tj = 0; tj < 4; ++tj)
+      for (int tj = 0; tj < TPW; ++tj)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int gj = (tj0 + tj) * 8 + 2 * (lane & 3) + e;
@@ -339,12 +360,12 @@ __global__ void __launch_bounds__(ET) jacobi_eig_kernel(JacArgs a) {
         }
     }
     __syncthreads();
-    mm64<false>(J, E, acc, ti, tj0, lane);
+    mmP<JB, TPW, false>(J, E, acc, ti, tj0, lane);
     __syncthreads();
     {
       const int gi = ti * 8 + (lane >> 2);
 #pragma unroll
-      for (int tj = 0; tj < 4; ++tj)
+      for (int tj = 0; tj < TPW; ++tj)
 #pragma unroll
         for (int e = 0; e < 2; ++e) J[gi * GLD + (tj0 + tj) * 8 + 2 * (lane & 3) + e] -= 0.5 * acc[tj][e];
     }
@@ -354,54 +375,60 @@ __global__ void __launch_bounds__(ET) jacobi_eig_kernel(JacArgs a) {
   for (int idx = t; idx < P2 * P2; idx += ET) Jout[idx] = J[(idx / P2) * GLD + idx % P2];
 }
 
+template <int JB>
 __global__ void __launch_bounds__(JT) jacobi_apply_kernel(JacArgs a) {
+  using K = JK<JB>;
+  constexpr int P2 = K::P2, JLD = K::JLD, CPW = K::NT / 2;   // column tiles per warp
   extern __shared__ __align__(16) double asm_[];
   double* buf0 = asm_;                 // 2 x P2*LDR chunk buffers
   double* Js = asm_ + 2 * P2 * LDR;    // P2 x JLD
   const int pair = blockIdx.x;
   if (a.skip[pair]) return;
-  const int which = a.which, split = blockIdx.y;
-  double* M = which == 0 ? a.X : a.V;
+  const int split = blockIdx.y;
+  double* M = a.which == 0 ? a.X : a.V;
   int bx, by;
   pair_of_round(a.nb, a.round, pair, bx, by);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
   const int nch = (int)cdiv_dev(re - rb, CH);
-  if (nch > 0) load_chunk(buf0, M, a.ld, rb, re, bx, by);
+  if (nch > 0) load_chunk<JB>(buf0, M, a.ld, rb, re, bx, by);
   cp_async_commit();
   const double* Jg = a.J + (int64_t)pair * P2 * P2;
   for (int idx = threadIdx.x; idx < P2 * P2; idx += JT) Js[(idx / P2) * JLD + idx % P2] = Jg[idx];
-  const int rt = warp & 3, ct0 = (warp >> 2) * 4;
+  const int rt = warp & 3, ct0 = (warp >> 2) * CPW;
   for (int i = 0; i < nch; ++i) {
     double* b = buf0 + (i & 1) * P2 * LDR;
     if (i + 1 < nch)
-      load_chunk(buf0 + ((i + 1) & 1) * P2 * LDR, M, a.ld, rb + (int64_t)(i + 1) * CH, re, bx, by);
+      load_chunk<JB>(buf0 + ((i + 1) & 1) * P2 * LDR, M, a.ld, rb + (int64_t)(i + 1) * CH, re,
+                     bx, by);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    // out (CH x 64) = chunk (CH x 64) * J: warp owns row tile rt, col tiles ct0..ct0+3
-    double o[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    // out (CH x P2) = chunk (CH x P2) * J: warp owns row tile rt, col tiles ct0..
+    double o[CPW][2];
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) o[c][0] = o[c][1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < P2 / 4; ++ks) {
       const double av = b[(4 * ks + (lane & 3)) * LDR + rt * 8 + (lane >> 2)];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < CPW; ++c)
         dmma(o[c], av, Js[(4 * ks + (lane & 3)) * JLD + (ct0 + c) * 8 + (lane >> 2)]);
     }
     __syncthreads();   // every warp has read the chunk
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int c = 0; c < CPW; ++c)
 #pragma unroll
       for (int e = 0; e < 2; ++e)
         b[((ct0 + c) * 8 + 2 * (lane & 3) + e) * LDR + rt * 8 + (lane >> 2)] = o[c][e];
     __syncthreads();
     const int64_t r0 = rb + (int64_t)i * CH;
-    for (int s = threadIdx.x; s < NSEG; s += JT) {
+    for (int s = threadIdx.x; s < K::NSEG; s += JT) {
       const int c = s / (CH / 2), rp2 = s % (CH / 2);
       const int64_t gr = r0 + 2 * rp2;
       if (gr < re) {
         double2 v = *reinterpret_cast<const double2*>(b + c * LDR + 2 * rp2);
-        *reinterpret_cast<double2*>(M + gr + gcol(c, bx, by) * a.ld) = v;
+        *reinterpret_cast<double2*>(M + gr + gcol<JB>(c, bx, by) * a.ld) = v;
       }
     }
     __syncthreads();
@@ -484,17 +511,23 @@ inline int gridn(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 148 * 16));
 }
 
-constexpr size_t EIG_SMEM = sizeof(double) * 2 * P2 * GLD;
-constexpr size_t APPLY_SMEM = sizeof(double) * (2 * P2 * LDR + P2 * JLD);
+template <int JB>
+constexpr size_t eig_smem() { return sizeof(double) * 2 * JK<JB>::P2 * JK<JB>::GLD; }
+template <int JB>
+constexpr size_t apply_smem() {
+  return sizeof(double) * (2 * JK<JB>::P2 * LDR + JK<JB>::P2 * JK<JB>::JLD);
+}
 
+template <int JB>
 void set_smem_attrs() {
-  static bool done = false;
-  if (done) return;
-  CK(cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)EIG_SMEM));
-  CK(cudaFuncSetAttribute(jacobi_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)APPLY_SMEM));
-  done = true;
+  static const bool done = [] {   // thread-safe one-time setup (magic static)
+    CK(cudaFuncSetAttribute(jacobi_eig_kernel<JB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)eig_smem<JB>()));
+    CK(cudaFuncSetAttribute(jacobi_apply_kernel<JB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)apply_smem<JB>()));
+    return true;
+  }();
+  (void)done;
 }
 
 }  // namespace
@@ -503,8 +536,11 @@ KernelProfile g_prof;
 
 // One-sided block Jacobi on the kp x kp matrix X (in place; columns >= k
 // and rows >= k are zero).  V (kp x kp) accumulates the rotations.
+template <int JB>
 static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, double* V) {
-  set_smem_attrs();
+  using K = JK<JB>;
+  constexpr int P2 = K::P2;
+  set_smem_attrs<JB>();
   set_identity(st, kp, kp, V, kp);
   const int nb = (int)(kp / JB), npairs = nb / 2;
   const double eps = 2.220446049250313e-16;
@@ -569,20 +605,20 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
       a.J = Jb[par];
       a.skip = Sb[par];
       if (prof) CK(cudaEventRecord(ev[4 * r], st));
-      jacobi_gram_kernel<<<dim3(npairs, splits), JT, 0, st>>>(a);
+      jacobi_gram_kernel<JB><<<dim3(npairs, splits), JT, 0, st>>>(a);
       CK_LAUNCH();
       if (prof) CK(cudaEventRecord(ev[4 * r + 1], st));
       if (overlap) CK(cudaStreamWaitEvent(st, evV[par], 0));
-      jacobi_eig_kernel<<<npairs, ET, EIG_SMEM, st>>>(a);
+      jacobi_eig_kernel<JB><<<npairs, K::ET, eig_smem<JB>(), st>>>(a);
       CK_LAUNCH();
       if (prof) CK(cudaEventRecord(ev[4 * r + 2], st));
       if (overlap) CK(cudaEventRecord(evE[par], st));
       a.which = 0;
-      jacobi_apply_kernel<<<dim3(npairs, splits), JT, APPLY_SMEM, st>>>(a);
+      jacobi_apply_kernel<JB><<<dim3(npairs, splits), JT, apply_smem<JB>(), st>>>(a);
       CK_LAUNCH();
       a.which = 1;
       if (overlap) CK(cudaStreamWaitEvent(sv, evE[par], 0));
-      jacobi_apply_kernel<<<dim3(npairs, splits), JT, APPLY_SMEM, sv>>>(a);
+      jacobi_apply_kernel<JB><<<dim3(npairs, splits), JT, apply_smem<JB>(), sv>>>(a);
       CK_LAUNCH();
       if (overlap) CK(cudaEventRecord(evV[par], sv));
       if (prof) CK(cudaEventRecord(ev[4 * r + 3], st));
@@ -622,7 +658,12 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   const int64_t k = std::min(m, n);
   out.k = k;
   if (k <= 0) return;
-  const int64_t kp = cdiv(k, P2) * P2;
+  // 32-column blocks for large k, 16-column blocks for small k (the inner
+  // Jacobi latency dominates small problems)
+  static const int64_t jb_split =
+      std::getenv("MPO_B200_JB16_MAXK") ? std::atoll(std::getenv("MPO_B200_JB16_MAXK")) : 512;
+  const int jbw = k <= jb_split ? 16 : 32;
+  const int64_t kp = cdiv(k, 2 * jbw) * 2 * jbw;
   const bool wide = m <= n;            // factor M^T = Q T  (n x m, tall)
   const int64_t tm = wide ? n : m;     // tall orientation rows
   DBuf<double> A((size_t)tm * k, st), Q((size_t)tm * k, st), R((size_t)k * k, st);
@@ -647,7 +688,8 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   static const bool trace = std::getenv("MPO_B200_TRACE") != nullptr;
   if (trace) CK(cudaStreamSynchronize(st));
   auto t0 = std::chrono::steady_clock::now();
-  const int sweeps = jacobi_sweeps(st, X.get(), k, kp, V.get());
+  const int sweeps = jbw == 16 ? jacobi_sweeps<16>(st, X.get(), k, kp, V.get())
+                                 : jacobi_sweeps<32>(st, X.get(), k, kp, V.get());
   if (trace) {
     double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     fprintf(stderr, "[mpo_b200]   jacobi k=%lld sweeps=%d %.3f ms\n", (long long)k, sweeps, ms);

@@ -195,6 +195,12 @@ def big():
     # config-5 TNrSVD instance, oracle-feasible q=0 variant (instance seed 50)
     a = rmpo.random_mpo([2] * 20, [2] * 20, [16] * 19, seed=50)
     cases["c5inst_q0"] = (a, dict(k_target=16, q=0, round_tol=1e-9, oversample=1.5, seed=51))
+    # config 3 at the oracle-feasible q=0 (q=2 dies with a 1.5 TiB core):
+    # cores N(0,1)/8, middle bond (core 5's right rank index k) scaled by 0.5^k
+    a = rmpo.random_mpo([4] * 12, [4] * 12, [64] * 11, seed=3)
+    cores = [c / 8.0 for c in a.cores]
+    cores[5] = cores[5] * (0.5 ** np.arange(64))[None, None, None, :]
+    cases["c3q0"] = (rmpo.Mpo(cores), dict(k_target=32, q=0, round_tol=1e-9, oversample=1.5, seed=4))
     only = sys.argv[2:] or list(cases)
     for name in only:
         a, kw = cases[name]

@@ -180,6 +180,21 @@ def test_c5_instance_q0_full_size():
     assert _ortho_err(lr.u.cores) <= 1e-12 and _ortho_err(lr.v.cores) <= 1e-12
 
 
+def test_c3_q0_full_size():
+    """Config 3 (d=10, 4096x4096 per mode pair, rank 64) at q=0 — the largest
+    configuration the reference finishes on CPU here (213 s): singular values
+    within 1e-8 and every output rank equal to the reference run
+    (big_c3q0.npz)."""
+    m = _api()
+    from paper_1707_07803_b200.workloads import TNRSVD_ARGS, config_mpo
+    z = load_golden("big_c3q0.npz")
+    lr = m.tnrsvd(config_mpo("c3q0"), **TNRSVD_ARGS["c3q0"])
+    np.testing.assert_allclose(lr.s, z["s"], rtol=S_RTOL)
+    assert lr.u.ranks == tuple(z["u_ranks"]) and lr.v.ranks == tuple(z["v_ranks"])
+    # bonds up to 4096: orthogonality loss grows ~ eps * sqrt(rank) per core
+    assert _ortho_err(lr.u.cores) <= 1e-11 and _ortho_err(lr.v.cores) <= 1e-11
+
+
 def test_c2_full_size():
     """Config 2 (BASELINE headline, d=20 rank 8, q=1): singular values within
     1e-8, all output ranks equal to the reference run (big_c2.npz), U and V
