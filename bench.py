@@ -112,6 +112,8 @@ class Clocks:
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
+        if os.environ.get("BENCH_NO_CLOCKS"):   # diagnostics only: no sampler
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -148,6 +150,7 @@ class Clocks:
         finally:
             os.unlink(self.path)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "sm_min_mhz": min(sm) if sm else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -249,12 +252,17 @@ def run_b200(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     with Clocks(local_rank) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         e0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             flush.zero_()
             s = step()
+            marks[i].record(stream)
         e1.record(stream)
         e1.synchronize()
+    step_ms = [e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i])
+                                             for i in range(1, args.steps)]
+    print("[bench] c2 device ms per step:", " ".join(f"{x:.1f}" for x in step_ms), file=sys.stderr)
     torch.cuda.synchronize()
     barrier()
     launches = _lib.launch_count() - l0

@@ -1,7 +1,10 @@
 // extern "C" boundary (include/mpo_b200.h): handles, argument validation,
 // exception -> status-code mapping.  See the header for the reference
 // functions each entry point replaces.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <string>
 
@@ -109,6 +112,22 @@ MPO_API int mpo_ctx_create(int device, void* stream, mpo_ctx** out) {
     CK(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = ~0ull;
     CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // grow the pool once up front (MPO_B200_POOL_RESERVE_GB, default 8):
+    // growing it mid-sweep maps new physical memory inside the timed path
+    static std::once_flag reserved[64];
+    std::call_once(reserved[device & 63], [&] {
+      const char* e = std::getenv("MPO_B200_POOL_RESERVE_GB");
+      const double gb = e ? std::atof(e) : 8.0;
+      size_t fr = 0, tot = 0;
+      CK(cudaMemGetInfo(&fr, &tot));
+      const size_t want = std::min((size_t)(gb * (1ull << 30)), fr / 2);
+      if (want > 0) {
+        void* p = nullptr;
+        CK(cudaMallocAsync(&p, want, nullptr));
+        CK(cudaFreeAsync(p, nullptr));
+        CK(cudaStreamSynchronize(nullptr));
+      }
+    });
     auto* c = new mpo_ctx;
     c->device = device;
     c->stream = static_cast<cudaStream_t>(stream);

@@ -65,7 +65,12 @@ struct SvdOut {
   DBuf<double> vh;      // k x n, column-major, ld = k
   int64_t k = 0;
 };
-void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ldm, SvdOut& out);
+// noise_floor: skip rotations whose coupling is below the O(eps ||M||)
+// backward-error level (singular values and the exact product U S Vh are
+// unaffected; U = ucarry / s is then not orthonormal for noise-level s, so
+// callers that need left vectors pass false)
+void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ldm, SvdOut& out,
+              bool noise_floor = false);
 
 }  // namespace mpob
 

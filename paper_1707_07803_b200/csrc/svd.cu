@@ -109,6 +109,8 @@ struct JacArgs {
   int* skip;       // npairs
   int* flag;       // any rotation in this sweep
   double tol;
+  const double* fro;  // ||X||_F (device scalar; invariant under rotations)
+  double floorc;      // pairs with g_pq^2 <= floorc ||X||_F^2 max(g_pp, g_qq) are noise
   int inner;       // inner (P2 x P2 Gram) Jacobi sweeps per outer round
   int* skiplog;    // profiling only: per (round, pair) skip flags, or null
   int which;       // apply: 0 = X, 1 = V
@@ -225,6 +227,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     if (i > j) G[i * GLD + j] = G[j * GLD + i];
   }
   __syncthreads();
+  const double gfl = a.floorc * (*a.fro) * (*a.fro);   // (c eps ||X||_F)^2
   {
     bool rot = false;
     for (int idx = t; idx < P2 * P2; idx += ET) {
@@ -232,7 +235,10 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
       if (i < j) {
         // sqrt before multiplying: G_ii * G_jj underflows for graded columns
         double d = sqrt(G[i * GLD + i]) * sqrt(G[j * GLD + j]);
-        if (d > 0.0 && fabs(G[i * GLD + j]) > a.tol * d) rot = true;
+        const double g = fabs(G[i * GLD + j]);
+        if (d > 0.0 && g > a.tol * d &&
+            g * g > gfl * fmax(G[i * GLD + i], G[j * GLD + j]))
+          rot = true;
       }
     }
     if (__syncthreads_or(rot)) s_skip = 0;
@@ -268,7 +274,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
         const int p = s_pq[r][t][0], q = s_pq[r][t][1];
         const double gpp = G[p * GLD + p], gqq = G[q * GLD + q], gpq = G[p * GLD + q];
         const double pq = gpp * gqq;
-        const bool rot = gpp > 0.0 && gqq > 0.0 &&
+        const bool rot = gpp > 0.0 && gqq > 0.0 && gpq * gpq > gfl * fmax(gpp, gqq) &&
                          (pq > 1e-280 ? gpq * gpq > a.tol * a.tol * pq
                                       : fabs(gpq) * rsqrt(gpp) * rsqrt(gqq) > a.tol);
         double c = 1.0, s = 0.0;
@@ -537,7 +543,8 @@ KernelProfile g_prof;
 // One-sided block Jacobi on the kp x kp matrix X (in place; columns >= k
 // and rows >= k are zero).  V (kp x kp) accumulates the rotations.
 template <int JB>
-static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, double* V) {
+static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, double* V,
+                         bool noise_floor) {
   using K = JK<JB>;
   constexpr int P2 = K::P2;
   set_smem_attrs<JB>();
@@ -560,16 +567,30 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   DBuf<int> skip2(npairs, st);
   double* Jb[2] = {J.get(), J2.get()};
   int* Sb[2] = {skip.get(), skip2.get()};
+  // noise floor: a pair whose coupling |g_pq| is below c eps ||X||_F times
+  // the larger column norm moves no singular value by more than O(eps ||X||),
+  // the backward error of any SVD (the reference's dgesdd included); without
+  // it, columns far below the noise level are orthogonalised to relative
+  // precision, which graded / rank-deficient blocks pay for in extra sweeps
+  static const double floor_mult =
+      std::getenv("MPO_B200_JFLOOR") ? std::atof(std::getenv("MPO_B200_JFLOOR")) : 1.0;
+  DBuf<double> fro(1, st);
+  frob_norm(st, X, kp * kp, fro.get());
   JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), Jb[0], Sb[0], flag.get(), tol,
-            inner, nullptr, 0};
+            fro.get(), noise_floor ? floor_mult * floor_mult * eps * eps : 0.0, inner, nullptr, 0};
   // profiling (bench.py roofline): CUDA events around every round kernel;
   // the V updates then stay on the main stream so the intervals are exact
   const bool prof = g_prof.on;
   DBuf<int> skiplog;
   std::vector<cudaEvent_t> ev;
-  if (prof) {
+  // MPO_B200_TRACE=2: rotating pairs per sweep (convergence diagnostics)
+  static const int trace_lvl =
+      std::getenv("MPO_B200_TRACE") ? std::atoi(std::getenv("MPO_B200_TRACE")) : 0;
+  if (prof || trace_lvl >= 2) {
     skiplog.alloc((size_t)(nb - 1) * npairs, st);
     a.skiplog = skiplog.get();
+  }
+  if (prof) {
     ev.resize(4 * (nb - 1));
     for (auto& e : ev) CK(cudaEventCreate(&e));
   }
@@ -626,6 +647,14 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
     note_launch(4 * (nb - 1));
     CK(cudaMemcpyAsync(&h_flag, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (trace_lvl >= 2) {
+      std::vector<int> sk((size_t)(nb - 1) * npairs);
+      CK(cudaMemcpy(sk.data(), skiplog.get(), sizeof(int) * sk.size(), cudaMemcpyDeviceToHost));
+      int64_t active = 0;
+      for (int x : sk) active += x == 0;
+      fprintf(stderr, "[mpo_b200]     k=%lld sweep %d: %lld of %lld pair blocks rotate\n",
+              (long long)k, sweep, (long long)active, (long long)sk.size());
+    }
     if (prof) {
       std::vector<int> sk((size_t)(nb - 1) * npairs);
       CK(cudaMemcpy(sk.data(), skiplog.get(), sizeof(int) * sk.size(), cudaMemcpyDeviceToHost));
@@ -654,7 +683,8 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   return sweeps;
 }
 
-void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ldm, SvdOut& out) {
+void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ldm, SvdOut& out,
+              bool noise_floor) {
   const int64_t k = std::min(m, n);
   out.k = k;
   if (k <= 0) return;
@@ -664,6 +694,8 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
       std::getenv("MPO_B200_JB16_MAXK") ? std::atoll(std::getenv("MPO_B200_JB16_MAXK")) : 512;
   const int jbw = k <= jb_split ? 16 : 32;
   const int64_t kp = cdiv(k, 2 * jbw) * 2 * jbw;
+  static const bool trace = std::getenv("MPO_B200_TRACE") != nullptr;
+  auto tq = std::chrono::steady_clock::now();
   const bool wide = m <= n;            // factor M^T = Q T  (n x m, tall)
   const int64_t tm = wide ? n : m;     // tall orientation rows
   DBuf<double> A((size_t)tm * k, st), Q((size_t)tm * k, st), R((size_t)k * k, st);
@@ -680,16 +712,37 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
     copy_matrix(st, m, n, M, ldm, A.get(), m);
   }
   householder_qr(st, tm, k, A.get(), tm, Q.get(), tm, R.get(), k);
-  // X = T^T (wide) or T (tall), zero padded to kp x kp
+  // Tall M = Q T: one more (k x k) QR, T^T = Q2 T2, so that the Jacobi runs
+  // on the lower-triangular T2^T (T = T2^T Q2^T).  One-sided Jacobi converges
+  // much faster on the transposed triangular factor (Drmac & Veselic, the
+  // orientation the wide case already has): measured 18 -> ~13 sweeps on
+  // config 2's 4096 x 2048 core, 33 -> ~14 on config 3's 4096 x 1024.
+  static const bool tall_lq =
+      std::getenv("MPO_B200_TALL_LQ") ? std::atoi(std::getenv("MPO_B200_TALL_LQ")) != 0 : true;
+  const bool lq = !wide && tall_lq;
+  DBuf<double> Q2;
+  if (lq) {
+    DBuf<double> A2((size_t)k * k, st);
+    int64_t dims[2] = {k, k};
+    int pr[2] = {1, 0};
+    permute(st, R.get(), A2.get(), 2, dims, pr);
+    Q2.alloc((size_t)k * k, st);
+    householder_qr(st, k, k, A2.get(), k, Q2.get(), k, R.get(), k);
+  }
+  // X = T^T (wide, or tall with the second QR) or T (tall), zero padded to kp x kp
   DBuf<double> X((size_t)kp * kp, st), V((size_t)kp * kp, st);
-  tri_transpose_kernel<<<gridn(kp * kp), 256, 0, st>>>(R.get(), k, k, kp, X.get(), wide ? 0 : 1);
+  tri_transpose_kernel<<<gridn(kp * kp), 256, 0, st>>>(R.get(), k, k, kp, X.get(),
+                                                        (wide || lq) ? 0 : 1);
   CK_LAUNCH();
   note_launch();
-  static const bool trace = std::getenv("MPO_B200_TRACE") != nullptr;
-  if (trace) CK(cudaStreamSynchronize(st));
+  if (trace) {
+    CK(cudaStreamSynchronize(st));
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq).count();
+    fprintf(stderr, "[mpo_b200]   precondition %lldx%lld %.3f ms\n", (long long)m, (long long)n, ms);
+  }
   auto t0 = std::chrono::steady_clock::now();
-  const int sweeps = jbw == 16 ? jacobi_sweeps<16>(st, X.get(), k, kp, V.get())
-                                 : jacobi_sweeps<32>(st, X.get(), k, kp, V.get());
+  const int sweeps = jbw == 16 ? jacobi_sweeps<16>(st, X.get(), k, kp, V.get(), noise_floor)
+                                 : jacobi_sweeps<32>(st, X.get(), k, kp, V.get(), noise_floor);
   if (trace) {
     double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     fprintf(stderr, "[mpo_b200]   jacobi k=%lld sweeps=%d %.3f ms\n", (long long)k, sweeps, ms);
@@ -717,18 +770,35 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   gather_cols_kernel<<<gridn(k * k), 256, 0, st>>>(V.get(), kp, k, perm.get(), k, Vs.get(), k);
   CK_LAUNCH();
   note_launch(2);
+  if (trace) CK(cudaStreamSynchronize(st));
+  auto ta = std::chrono::steady_clock::now();
   out.ucarry.alloc((size_t)m * k, st);
   out.vh.alloc((size_t)k * n, st);
+  if (trace) {
+    CK(cudaStreamSynchronize(st));
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta).count();
+    fprintf(stderr, "[mpo_b200]   outalloc %lldx%lld %.3f ms\n", (long long)m, (long long)n, ms);
+    ta = std::chrono::steady_clock::now();
+  }
   if (wide) {
     // M = X Q^T, X Vs = Ys:  Ucarry = Ys (m = k rows),  Vh = Vs^T Q^T = (Q Vs)^T
     copy_matrix(st, k, k, Ys.get(), k, out.ucarry.get(), m);
     dgemm(st, true, true, k, n, k, 1.0, Vs.get(), k, Q.get(), tm, 0.0, out.vh.get(), k);
+  } else if (lq) {
+    // M = Q X Q2^T:  Ucarry = Q Ys,  Vh = (Q2 Vs)^T
+    dgemm(st, false, false, m, k, k, 1.0, Q.get(), tm, Ys.get(), k, 0.0, out.ucarry.get(), m);
+    dgemm(st, true, true, k, k, k, 1.0, Vs.get(), k, Q2.get(), k, 0.0, out.vh.get(), k);
   } else {
     // M = Q X:  Ucarry = Q Ys,  Vh = Vs^T
     dgemm(st, false, false, m, k, k, 1.0, Q.get(), tm, Ys.get(), k, 0.0, out.ucarry.get(), m);
     int64_t dims[2] = {k, k};
     int pr[2] = {1, 0};
     permute(st, Vs.get(), out.vh.get(), 2, dims, pr);
+  }
+  if (trace) {
+    CK(cudaStreamSynchronize(st));
+    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta).count();
+    fprintf(stderr, "[mpo_b200]   finish %lldx%lld %.3f ms\n", (long long)m, (long long)n, ms);
   }
 }
 

@@ -201,7 +201,7 @@ void r2l(cudaStream_t st, Cores& cores, bool has_tol, double tol) {
       SvdOut o;
       {
         Trace tr(st, "svd", R, N);
-        svd_thin(st, R, N, c.p(), R, o);
+        svd_thin(st, R, N, c.p(), R, o, /*noise_floor=*/true);
       }
       std::vector<double> s(o.k);
       CK(cudaMemcpyAsync(s.data(), o.s.get(), sizeof(double) * o.k, cudaMemcpyDeviceToHost, st));
