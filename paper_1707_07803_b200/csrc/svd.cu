@@ -524,6 +524,15 @@ constexpr size_t apply_smem() {
   return sizeof(double) * (2 * JK<JB>::P2 * LDR + JK<JB>::P2 * JK<JB>::JLD);
 }
 
+void sort_smem_attr() {
+  static const bool done = [] {
+    CK(cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            8192 * (int)(sizeof(double) + sizeof(int))));
+    return true;
+  }();
+  (void)done;
+}
+
 template <int JB>
 void set_smem_attrs() {
   static const bool done = [] {   // thread-safe one-time setup (magic static)
@@ -616,9 +625,57 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
     for (int i = 0; i < 2; ++i) CK(cudaEventRecord(evV[i], st));
     CK(cudaStreamWaitEvent(sv, evV[0], 0));   // V = I is ready
   }
+  // MPO_B200_SORT_SWEEPS=n: before sweeps 1..n, reorder the k live columns
+  // of X (and V) by decreasing norm (de Rijk ordering)
+  static const int sort_sweeps =
+      std::getenv("MPO_B200_SORT_SWEEPS") ? std::atoi(std::getenv("MPO_B200_SORT_SWEEPS")) : 3;
+  static const int sort_from =
+      std::getenv("MPO_B200_SORT_FROM") ? std::atoi(std::getenv("MPO_B200_SORT_FROM")) : 1;
+  DBuf<double> X2, V2, nrm;
+  DBuf<int> prm;
+  int np2 = 1;
+  while (np2 < k) np2 <<= 1;
+  const bool sorting = sort_sweeps > 0 && np2 <= 8192;
+  if (sorting) {
+    X2.alloc((size_t)kp * kp, st);
+    V2.alloc((size_t)kp * kp, st);
+    nrm.alloc(kp, st);
+    prm.alloc(kp, st);
+    sort_smem_attr();
+  }
   int h_flag = 0, sweeps = 0;
   int64_t rr = 0;   // global round counter (buffer parity across sweeps)
   for (int sweep = 0; sweep < 60; ++sweep) {
+    if (sorting && sweep >= sort_from && sweep < sort_from + sort_sweeps) {
+      if (overlap) {
+        CK(cudaEventRecord(evV[(rr + 1) & 1], sv));
+        CK(cudaStreamWaitEvent(st, evV[(rr + 1) & 1], 0));
+      }
+      col_norms_kernel<<<(int)cdiv(k, 8), 256, 0, st>>>(a.X, kp, kp, k, nrm.get());
+      CK_LAUNCH();
+      sort_desc_kernel<<<1, 1024, (size_t)np2 * (sizeof(double) + sizeof(int)), st>>>(
+          nrm.get(), (int)k, np2, nrm.get(), prm.get());
+      CK_LAUNCH();
+      double* nx = a.X == X ? X2.get() : X;
+      double* nv = a.V == V ? V2.get() : V;
+      gather_cols_kernel<<<gridn(kp * k), 256, 0, st>>>(a.X, kp, kp, prm.get(), k, nx, kp);
+      CK_LAUNCH();
+      gather_cols_kernel<<<gridn(kp * k), 256, 0, st>>>(a.V, kp, kp, prm.get(), k, nv, kp);
+      CK_LAUNCH();
+      note_launch(4);
+      if (kp > k) {
+        CK(cudaMemcpyAsync(nx + k * kp, a.X + k * kp, sizeof(double) * (kp - k) * kp,
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(nv + k * kp, a.V + k * kp, sizeof(double) * (kp - k) * kp,
+                           cudaMemcpyDeviceToDevice, st));
+      }
+      a.X = nx;
+      a.V = nv;
+      if (overlap) {
+        CK(cudaEventRecord(evV[(rr + 1) & 1], st));
+        CK(cudaStreamWaitEvent(sv, evV[(rr + 1) & 1], 0));
+      }
+    }
     CK(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
     for (int r = 0; r < nb - 1; ++r, ++rr) {
       const int par = (int)(rr & 1);
@@ -678,6 +735,10 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
     // the main stream continues only after the last V update
     CK(cudaEventRecord(evV[0], sv));
     CK(cudaStreamWaitEvent(st, evV[0], 0));
+  }
+  if (a.X != X) {   // sorted copies live in the scratch buffers
+    CK(cudaMemcpyAsync(X, a.X, sizeof(double) * kp * kp, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(V, a.V, sizeof(double) * kp * kp, cudaMemcpyDeviceToDevice, st));
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return sweeps;
