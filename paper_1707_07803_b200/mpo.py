@@ -198,7 +198,9 @@ class DeviceMpo:
         return out
 
     def to_host(self) -> Mpo:
-        return Mpo([np.ascontiguousarray(self.core(k)) for k in range(self.num_cores)])
+        # cores stay in the device's F order (same values and shapes; a C-order
+        # copy would be a strided transpose of every core on the host)
+        return Mpo([self.core(k) for k in range(self.num_cores)])
 
     def free(self):
         if self.handle is not None and self.handle.value:
