@@ -112,6 +112,7 @@ struct JacArgs {
   const double* fro;  // ||X||_F (device scalar; invariant under rotations)
   double floorc;      // pairs with g_pq^2 <= floorc ||X||_F^2 max(g_pp, g_qq) are noise
   int inner;       // inner (P2 x P2 Gram) Jacobi sweeps per outer round
+  int ns_steps;    // Newton-Schulz re-orthogonalisation steps on J
   int* skiplog;    // profiling only: per (round, pair) skip flags, or null
   int which;       // apply: 0 = X, 1 = V
 };
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
   constexpr int NW = ET / 32, TPW = K::NT * K::NT / NW;
   double* E = G;
   const int ti = warp % K::NT, tj0 = (warp / K::NT) * TPW;
-  for (int it = 0; it < 2; ++it) {
+  for (int it = 0; it < a.ns_steps; ++it) {
     __syncthreads();
     double acc[TPW][2];
     mmP<JB, TPW, true>(J, J, acc, ti, tj0, lane);
@@ -568,6 +569,11 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   DBuf<int> skip(npairs, st), flag(1, st);
   static const int inner =
       std::getenv("MPO_B200_INNER") ? std::atoi(std::getenv("MPO_B200_INNER")) : 1;
+  // one step suffices: every rotation is orthogonal to O(eps) (FP64
+  // renormalised), so J's defect after one inner sweep is ~P2 eps and one
+  // quadratic step takes it to rounding level
+  static const int ns_steps =
+      std::getenv("MPO_B200_NS") ? std::atoi(std::getenv("MPO_B200_NS")) : 1;
   // J and skip flags are double-buffered by round parity: the V updates of
   // round r run on a second stream, overlapping the gram / eig of round
   // r+1 (V is never read by the iteration itself), and the eig of round
@@ -586,7 +592,8 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   DBuf<double> fro(1, st);
   frob_norm(st, X, kp * kp, fro.get());
   JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), Jb[0], Sb[0], flag.get(), tol,
-            fro.get(), noise_floor ? floor_mult * floor_mult * eps * eps : 0.0, inner, nullptr, 0};
+            fro.get(), noise_floor ? floor_mult * floor_mult * eps * eps : 0.0, inner, ns_steps,
+            nullptr, 0};
   // profiling (bench.py roofline): CUDA events around every round kernel;
   // the V updates then stay on the main stream so the intervals are exact
   const bool prof = g_prof.on;
