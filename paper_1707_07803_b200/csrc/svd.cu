@@ -195,6 +195,11 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
   double* G = dsm;              // P2 x GLD
   double* J = dsm + P2 * GLD;   // P2 x GLD
   __shared__ unsigned char s_pq[P2 - 1][NPR][2];
+  // G is kept as its upper triangle only (entry (a, b) at min*GLD + max):
+  // the 2x2 block updates then cover NPR(NPR+1)/2 blocks instead of NPR^2.
+  // s_blk lists them, off-diagonal (u < v) first, diagonal last.
+  constexpr int NBLK = NPR * (NPR + 1) / 2;
+  __shared__ unsigned char s_blk[NBLK][2];
   __shared__ double rc[NPR], rs[NPR], rdp[NPR], rdq[NPR];
   __shared__ int rflag[NPR];
   __shared__ int s_skip;
@@ -221,13 +226,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     }
   }
   if (t == 0) s_skip = 1;
-  __syncthreads();
-  // symmetrise from the upper triangle
-  for (int idx = t; idx < P2 * P2; idx += ET) {
-    int i = idx / P2, j = idx % P2;
-    if (i > j) G[i * GLD + j] = G[j * GLD + i];
-  }
-  __syncthreads();
+  __syncthreads();   // only the upper triangle of G is read from here on
   const double gfl = a.floorc * (*a.fro) * (*a.fro);   // (c eps ||X||_F)^2
   {
     bool rot = false;
@@ -266,6 +265,17 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     pair_of_round(P2, r, i, p, q);
     s_pq[r][i][0] = (unsigned char)min(p, q);
     s_pq[r][i][1] = (unsigned char)max(p, q);
+  }
+  for (int idx = t; idx < NPR * NPR; idx += ET) {
+    const int u = idx / NPR, v = idx % NPR;
+    if (u < v) {   // position of (u, v) among the off-diagonal blocks, row-major
+      const int o = u * NPR - u * (u + 1) / 2 + (v - u - 1);
+      s_blk[o][0] = (unsigned char)u;
+      s_blk[o][1] = (unsigned char)v;
+    } else if (u == v) {
+      s_blk[NPR * (NPR - 1) / 2 + u][0] = (unsigned char)u;
+      s_blk[NPR * (NPR - 1) / 2 + u][1] = (unsigned char)u;
+    }
   }
   __syncthreads();
   for (int sweep = 0; sweep < a.inner; ++sweep) {
@@ -308,28 +318,28 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
         any |= rot;
       }
       __syncthreads();
-#pragma unroll
-      for (int h = 0; h < NPR * NPR / ET; ++h) {
-        const int idx = t + h * ET, u = idx / NPR, v = idx % NPR;
+      for (int idx = t; idx < NBLK; idx += ET) {
+        const int u = s_blk[idx][0], v = s_blk[idx][1];
         if (!(rflag[u] | rflag[v])) continue;
         const int pu = s_pq[r][u][0], qu = s_pq[r][u][1];
         if (u == v) {
           G[pu * GLD + pu] = rdp[u];
           G[qu * GLD + qu] = rdq[u];
-          G[pu * GLD + qu] = 0.0;
-          G[qu * GLD + pu] = 0.0;
+          G[pu * GLD + qu] = 0.0;   // pu < qu
           continue;
         }
         const int pv = s_pq[r][v][0], qv = s_pq[r][v][1];
         const double cu = rc[u], su = rs[u], cv = rc[v], sv = rs[v];
-        const double b00 = G[pu * GLD + pv], b01 = G[pu * GLD + qv];
-        const double b10 = G[qu * GLD + pv], b11 = G[qu * GLD + qv];
+        // entry (a, b) of the symmetric G lives at min(a,b)*GLD + max(a,b)
+        const int a00 = min(pu, pv) * GLD + max(pu, pv), a01 = min(pu, qv) * GLD + max(pu, qv);
+        const int a10 = min(qu, pv) * GLD + max(qu, pv), a11 = min(qu, qv) * GLD + max(qu, qv);
+        const double b00 = G[a00], b01 = G[a01], b10 = G[a10], b11 = G[a11];
         const double x00 = cv * b00 - sv * b01, x01 = sv * b00 + cv * b01;
         const double x10 = cv * b10 - sv * b11, x11 = sv * b10 + cv * b11;
-        G[pu * GLD + pv] = cu * x00 - su * x10;
-        G[pu * GLD + qv] = cu * x01 - su * x11;
-        G[qu * GLD + pv] = su * x00 + cu * x10;
-        G[qu * GLD + qv] = su * x01 + cu * x11;
+        G[a00] = cu * x00 - su * x10;
+        G[a01] = cu * x01 - su * x11;
+        G[a10] = su * x00 + cu * x10;
+        G[a11] = su * x01 + cu * x11;
       }
 #pragma unroll
       for (int h = 0; h < P2 * NPR / ET; ++h) {
