@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libmpo_b200.so")
+# MPO_B200_LIB: alternative build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("MPO_B200_LIB") or os.path.join(HERE, "lib", "libmpo_b200.so")
 
 MPO_OK, MPO_EVALUE, MPO_ECUDA, MPO_ENOMEM, MPO_EINTERNAL = range(5)
 

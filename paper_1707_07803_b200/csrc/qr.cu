@@ -254,14 +254,12 @@ struct ClusterPanelArgs {
 
 __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPanelArgs p) {
   extern __shared__ double chunk[];  // rpc x w, column-major
-  __shared__ double s_part, s_alpha;
-  __shared__ double s_wpart[QR_NB];
+  __shared__ double s_pub[2][2 * QR_NB];   // published partials (dots | row jj), by parity
+  __shared__ double s_tot[2 * QR_NB];
   __shared__ double s_w[QR_NB];
   __shared__ double s_vtv[QR_NB * QR_NB];
   __shared__ double s_tau[QR_NB];
-  __shared__ double red[QR_THREADS / 32];
-  __shared__ double s_scal, s_tauj, s_beta;
-  __shared__ double s_red[16 * QR_NB];
+  __shared__ double s_red[16 * 2 * QR_NB];
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks(), c = (int)cluster.block_rank();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -274,88 +272,73 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
     chunk[r + col * ld] = p.A[(r0 + r) + col * p.lda];
   }
   __syncthreads();
+  // One cluster barrier per column: the norm of column jj and the dots
+  // x^T a_c of its sub-diagonal part with every later panel column are
+  // reduced together (plus the owner's row-jj entries), since with
+  // v = [1; scal x] the reflector's w_c = tau (a_jj,c + scal x^T a_c).  The
+  // published partials are double-buffered by column parity: a rank reads
+  // buffer jj&1 after barrier jj and has passed barrier jj+1 before anyone
+  // rewrites it (column jj+2).
   for (int jj = 0; jj < w; ++jj) {
-    double s = 0.0;
-    for (int r = t; r < nr; r += QR_THREADS) {
-      int64_t gr = r0 + r;
-      if (gr > jj) { double x = chunk[r + jj * ld]; s = fma(x, x, s); }
-      if (gr == jj) s_alpha = chunk[r + jj * ld];
-    }
-    s = warp_sum(s);
-    if (lane == 0) red[warp] = s;
-    __syncthreads();
-    if (t == 0) {
-      double tot = 0.0;
-      for (int i = 0; i < QR_THREADS / 32; ++i) tot += red[i];
-      s_part = tot;
-    }
-    cluster.sync();
-    if (warp == 0) {
-      // all ranks' partials fetched concurrently over DSMEM, fixed xor-tree sum
-      double sig = lane < CS ? *cluster.map_shared_rank(&s_part, lane) : 0.0;
-      const double al = *cluster.map_shared_rank(&s_alpha, (int)(jj / p.rpc));
-      sig = warp_sum(sig);
-      double tau = 0.0, beta = al, scal = 0.0;
-      if (sig != 0.0) {
-        double nrm = sqrt(fma(al, al, sig));
-        beta = al >= 0.0 ? -nrm : nrm;
-        tau = (beta - al) / beta;
-        scal = 1.0 / (al - beta);
-      }
-      s_tauj = tau; s_beta = beta; s_scal = scal;
-      s_tau[jj] = tau;
-    }
-    __syncthreads();
-    const double scal = s_scal;
-    for (int r = t; r < nr; r += QR_THREADS)
-      if (r0 + r > jj) chunk[r + jj * ld] *= scal;
-    __syncthreads();
-    const int ncols = w - jj - 1;
-    // partial w = v^T A_panel: each warp owns 4 columns (4 independent chains)
+    const int ncols = w - jj;            // slot 0: column jj itself (its norm)
+    double* pub = s_pub[jj & 1];
     for (int col0 = warp * 4; col0 < ncols; col0 += QR_THREADS / 8) {
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       for (int r = lane; r < nr; r += 32) {
-        const int64_t gr = r0 + r;
-        if (gr >= jj) {
-          const double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
+        if (r0 + r > jj) {
+          const double x = chunk[r + jj * ld];
 #pragma unroll
           for (int u = 0; u < 4; ++u)
-            if (col0 + u < ncols) acc[u] = fma(v, chunk[r + (jj + 1 + col0 + u) * ld], acc[u]);
+            if (col0 + u < ncols) acc[u] = fma(x, chunk[r + (jj + col0 + u) * ld], acc[u]);
         }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const double sum = warp_sum(acc[u]);
-        if (lane == 0 && col0 + u < ncols) s_wpart[col0 + u] = sum;
+        if (lane == 0 && col0 + u < ncols) pub[col0 + u] = sum;
       }
     }
+    const bool owner = jj >= r0 && jj < r0 + nr;
+    for (int u = t; u < ncols; u += QR_THREADS)
+      pub[QR_NB + u] = owner ? chunk[(jj - r0) + (jj + u) * ld] : 0.0;
     cluster.sync();
-    if (ncols > 0) {
-      const double tau = s_tauj;
-      // gather every rank's partials concurrently, then sum in rank order
-      for (int idx = t; idx < CS * ncols; idx += QR_THREADS) {
-        const int rk = idx / ncols, col = idx % ncols;
-        s_red[rk * QR_NB + col] = cluster.map_shared_rank(s_wpart, rk)[col];
-      }
-      __syncthreads();
-      if (t < ncols) {
-        double tot = 0.0;
-        for (int i = 0; i < CS; ++i) tot += s_red[i * QR_NB + t];
-        s_w[t] = tot * tau;
-      }
-      __syncthreads();
-      // rank-1 update of the remaining panel columns (no integer division:
-      // each thread keeps its rows and walks the columns)
-      for (int r = t; r < nr; r += QR_THREADS) {
-        const int64_t gr = r0 + r;
-        if (gr < jj) continue;
-        const double v = (gr == jj) ? 1.0 : chunk[r + jj * ld];
-        double* rowp = chunk + r + (jj + 1) * ld;
-        for (int col = 0; col < ncols; ++col) rowp[col * ld] -= v * s_w[col];
-      }
+    // gather every rank's partials concurrently, then sum in rank order
+    for (int idx = t; idx < CS * 2 * ncols; idx += QR_THREADS) {
+      const int rk = idx / (2 * ncols), e = idx % (2 * ncols);
+      const int slot = e < ncols ? e : QR_NB + (e - ncols);
+      s_red[rk * 2 * QR_NB + slot] = cluster.map_shared_rank(pub, rk)[slot];
     }
-    for (int r = t; r < nr; r += QR_THREADS)
-      if (r0 + r == jj) chunk[r + jj * ld] = s_beta;
+    __syncthreads();
+    for (int e = t; e < 2 * ncols; e += QR_THREADS) {
+      const int slot = e < ncols ? e : QR_NB + (e - ncols);
+      double tot = 0.0;
+      for (int i = 0; i < CS; ++i) tot += s_red[i * 2 * QR_NB + slot];
+      s_tot[slot] = tot;
+    }
+    __syncthreads();
+    // every thread derives the reflector (same inputs, same arithmetic)
+    const double sig = s_tot[0], al = s_tot[QR_NB];
+    double tau = 0.0, beta = al, scal = 0.0;
+    if (sig != 0.0) {
+      const double nrm = sqrt(fma(al, al, sig));
+      beta = al >= 0.0 ? -nrm : nrm;
+      tau = (beta - al) / beta;
+      scal = 1.0 / (al - beta);
+    }
+    if (t == 0) s_tau[jj] = tau;
+    for (int c = 1 + t; c < ncols; c += QR_THREADS)
+      s_w[c] = tau * fma(scal, s_tot[c], s_tot[QR_NB + c]);
+    __syncthreads();
+    // v = [1; scal x]; rank-1 update of the later panel columns
+    for (int r = t; r < nr; r += QR_THREADS) {
+      const int64_t gr = r0 + r;
+      if (gr < jj) continue;
+      double* rowp = chunk + r + jj * ld;
+      double v = 1.0;
+      if (gr > jj) { v = rowp[0] * scal; rowp[0] = v; }
+      else rowp[0] = beta;
+      for (int c = 1; c < ncols; ++c) rowp[c * ld] -= v * s_w[c];
+    }
     __syncthreads();
   }
   for (int idx = t; idx < nr * w; idx += QR_THREADS) {

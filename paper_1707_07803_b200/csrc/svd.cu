@@ -46,7 +46,13 @@ struct JK {
   static constexpr int GLD = P2 + 1;       // Gram / J row stride in the eig kernel
   static constexpr int JLD = P2 + 4;       // J row stride in the apply kernel
   static constexpr int NSEG = P2 * 32 / 2; // 16-byte segments per 32-row chunk
-  static constexpr int ET = P2 == 64 ? 512 : 256;   // eig kernel threads
+#ifndef MPO_EIG_ET64
+#define MPO_EIG_ET64 512
+#endif
+#ifndef MPO_EIG_ET32
+#define MPO_EIG_ET32 256
+#endif
+  static constexpr int ET = P2 == 64 ? MPO_EIG_ET64 : MPO_EIG_ET32;   // eig kernel threads
 };
 constexpr int CH = 32;        // rows per streamed chunk
 constexpr int LDR = CH + 4;   // chunk column stride (doubles): conflict-free DMMA fragments
