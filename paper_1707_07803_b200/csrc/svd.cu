@@ -44,7 +44,6 @@ struct JK {
   static constexpr int NPR = JB_;          // rotations per inner round
   static constexpr int NT = P2 / 8;        // 8x8 tiles per dimension
   static constexpr int GLD = P2 + 1;       // Gram / J row stride in the eig kernel
-  static constexpr int JLD = P2 + 4;       // J row stride in the apply kernel
   static constexpr int NSEG = P2 * 32 / 2; // 16-byte segments per 32-row chunk
 #ifndef MPO_EIG_ET64
 #define MPO_EIG_ET64 512
@@ -398,13 +397,20 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
   for (int idx = t; idx < P2 * P2; idx += ET) Jout[idx] = J[(idx / P2) * GLD + idx % P2];
 }
 
+// M[:, pair columns] <- M[:, pair columns] J for this CTA's rows, in place.
+// The J operand is constant over all chunks, so each warp keeps its B
+// fragments (2 column tiles x P2/4 k-steps) in registers and only the A
+// fragments come from shared memory; results go straight from the
+// accumulators to global memory (each store instruction covers 4 columns x
+// 8 consecutive rows: full 32-byte sectors).  Chunks stream through a
+// 3-buffer cp.async ring with one barrier per chunk.
 template <int JB>
-__global__ void __launch_bounds__(JT) jacobi_apply_kernel(JacArgs a) {
+__global__ void __launch_bounds__(JT, 2) jacobi_apply_kernel(JacArgs a) {
   using K = JK<JB>;
-  constexpr int P2 = K::P2, JLD = K::JLD, CPW = K::NT / 2;   // column tiles per warp
-  extern __shared__ __align__(16) double asm_[];
-  double* buf0 = asm_;                 // 2 x P2*LDR chunk buffers
-  double* Js = asm_ + 2 * P2 * LDR;    // P2 x JLD
+  constexpr int P2 = K::P2, NT = K::NT, NBUF = 3;
+  constexpr int CTW = 2;                        // column tiles per warp
+  constexpr int RTW = (CH / 8) * NT / (8 * CTW); // row tiles per warp (2 for P2=64, 1 for 32)
+  extern __shared__ __align__(16) double asm_[];   // NBUF x P2*LDR chunk buffers
   const int pair = blockIdx.x;
   if (a.skip[pair]) return;
   const int split = blockIdx.y;
@@ -414,47 +420,58 @@ __global__ void __launch_bounds__(JT) jacobi_apply_kernel(JacArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
   const int nch = (int)cdiv_dev(re - rb, CH);
-  if (nch > 0) load_chunk<JB>(buf0, M, a.ld, rb, re, bx, by);
-  cp_async_commit();
-  const double* Jg = a.J + (int64_t)pair * P2 * P2;
-  for (int idx = threadIdx.x; idx < P2 * P2; idx += JT) Js[(idx / P2) * JLD + idx % P2] = Jg[idx];
-  const int rt = warp & 3, ct0 = (warp >> 2) * CPW;
-  for (int i = 0; i < nch; ++i) {
-    double* b = buf0 + (i & 1) * P2 * LDR;
-    if (i + 1 < nch)
-      load_chunk<JB>(buf0 + ((i + 1) & 1) * P2 * LDR, M, a.ld, rb + (int64_t)(i + 1) * CH, re,
-                     bx, by);
+  for (int s = 0; s < NBUF - 1; ++s) {
+    if (s < nch) load_chunk<JB>(asm_ + s * P2 * LDR, M, a.ld, rb + (int64_t)s * CH, re, bx, by);
     cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    // out (CH x P2) = chunk (CH x P2) * J: warp owns row tile rt, col tiles ct0..
-    double o[CPW][2];
+  }
+  const int ct0 = (warp % (NT / CTW)) * CTW, rt0 = (warp / (NT / CTW)) * RTW;
+  const double* Jg = a.J + (int64_t)pair * P2 * P2;   // row-major P2 x P2
+  double bj[CTW][P2 / 4];
 #pragma unroll
-    for (int c = 0; c < CPW; ++c) o[c][0] = o[c][1] = 0.0;
+  for (int c = 0; c < CTW; ++c)
+#pragma unroll
+    for (int ks = 0; ks < P2 / 4; ++ks)
+      bj[c][ks] = Jg[(4 * ks + (lane & 3)) * P2 + (ct0 + c) * 8 + (lane >> 2)];
+  // output columns of this lane (2 per column tile) and their global offsets
+  int64_t coff[CTW][2];
+#pragma unroll
+  for (int c = 0; c < CTW; ++c)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) coff[c][e] = gcol<JB>((ct0 + c) * 8 + 2 * (lane & 3) + e, bx, by) * a.ld;
+  for (int i = 0; i < nch; ++i) {
+    cp_async_wait<NBUF - 2>();
+    __syncthreads();   // chunk i landed; every warp is done with chunk i-1
+    if (i + NBUF - 1 < nch)
+      load_chunk<JB>(asm_ + ((i + NBUF - 1) % NBUF) * P2 * LDR, M, a.ld,
+                     rb + (int64_t)(i + NBUF - 1) * CH, re, bx, by);
+    cp_async_commit();
+    const double* b = asm_ + (i % NBUF) * P2 * LDR;
+    double o[RTW][CTW][2];
+#pragma unroll
+    for (int r = 0; r < RTW; ++r)
+#pragma unroll
+      for (int c = 0; c < CTW; ++c) o[r][c][0] = o[r][c][1] = 0.0;
 #pragma unroll
     for (int ks = 0; ks < P2 / 4; ++ks) {
-      const double av = b[(4 * ks + (lane & 3)) * LDR + rt * 8 + (lane >> 2)];
+      double av[RTW];
 #pragma unroll
-      for (int c = 0; c < CPW; ++c)
-        dmma(o[c], av, Js[(4 * ks + (lane & 3)) * JLD + (ct0 + c) * 8 + (lane >> 2)]);
+      for (int r = 0; r < RTW; ++r) av[r] = b[(4 * ks + (lane & 3)) * LDR + (rt0 + r) * 8 + (lane >> 2)];
+#pragma unroll
+      for (int r = 0; r < RTW; ++r)
+#pragma unroll
+        for (int c = 0; c < CTW; ++c) dmma(o[r][c], av[r], bj[c][ks]);
     }
-    __syncthreads();   // every warp has read the chunk
-#pragma unroll
-    for (int c = 0; c < CPW; ++c)
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        b[((ct0 + c) * 8 + 2 * (lane & 3) + e) * LDR + rt * 8 + (lane >> 2)] = o[c][e];
-    __syncthreads();
     const int64_t r0 = rb + (int64_t)i * CH;
-    for (int s = threadIdx.x; s < K::NSEG; s += JT) {
-      const int c = s / (CH / 2), rp2 = s % (CH / 2);
-      const int64_t gr = r0 + 2 * rp2;
+#pragma unroll
+    for (int r = 0; r < RTW; ++r) {
+      const int64_t gr = r0 + (rt0 + r) * 8 + (lane >> 2);
       if (gr < re) {
-        double2 v = *reinterpret_cast<const double2*>(b + c * LDR + 2 * rp2);
-        *reinterpret_cast<double2*>(M + gr + gcol<JB>(c, bx, by) * a.ld) = v;
+#pragma unroll
+        for (int c = 0; c < CTW; ++c)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) M[gr + coff[c][e]] = o[r][c][e];
       }
     }
-    __syncthreads();
   }
 }
 
@@ -538,7 +555,7 @@ template <int JB>
 constexpr size_t eig_smem() { return sizeof(double) * 2 * JK<JB>::P2 * JK<JB>::GLD; }
 template <int JB>
 constexpr size_t apply_smem() {
-  return sizeof(double) * (2 * JK<JB>::P2 * LDR + JK<JB>::P2 * JK<JB>::JLD);
+  return sizeof(double) * 3 * JK<JB>::P2 * LDR;   // 3-buffer chunk ring
 }
 
 void sort_smem_attr() {
