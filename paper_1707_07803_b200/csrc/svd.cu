@@ -88,19 +88,31 @@ __device__ __forceinline__ int64_t gcol(int c, int bx, int by) {
   return c < JB ? (int64_t)bx * JB + c : (int64_t)by * JB + (c - JB);
 }
 
-// issue the cp.async loads of rows [r0, r0 + CH) of the pair's P2 columns
+// cp.async loader of rows [r0, r0 + CH) of the pair's P2 columns.  Each
+// thread's 16-byte segments sit at fixed (column, row-pair) positions of
+// every chunk, so their column base pointers and shared-memory offsets are
+// computed once per kernel; a chunk load is then PER address adds.
 template <int JB>
-__device__ __forceinline__ void load_chunk(double* buf, const double* M, int64_t ld,
-                                           int64_t r0, int64_t rend, int bx, int by) {
-  using K = JK<JB>;
-  for (int s = threadIdx.x; s < K::NSEG; s += JT) {
-    const int c = s / (CH / 2), rp = s % (CH / 2);
-    const int64_t gr = r0 + 2 * rp;
-    const bool ok = gr < rend;  // rows come in pairs (kp is even)
-    const double* src = M + (ok ? gr : 0) + gcol<JB>(c, bx, by) * ld;
-    cp_async16(buf + c * LDR + 2 * rp, src, ok ? 16 : 0);
+struct ChunkLoader {
+  static constexpr int PER = JK<JB>::NSEG / JT;
+  const double* src[PER];
+  int dst[PER];
+  int rp2;
+  __device__ __forceinline__ ChunkLoader(const double* M, int64_t ld, int bx, int by) {
+    rp2 = 2 * (threadIdx.x % (CH / 2));   // JT is a multiple of CH/2
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const int c = (threadIdx.x + j * JT) / (CH / 2);
+      src[j] = M + gcol<JB>(c, bx, by) * ld + rp2;
+      dst[j] = c * LDR + rp2;
+    }
   }
-}
+  __device__ __forceinline__ void load(double* buf, int64_t r0, int64_t rend) const {
+    const bool ok = r0 + rp2 < rend;   // rows come in pairs (kp is even)
+#pragma unroll
+    for (int j = 0; j < PER; ++j) cp_async16(buf + dst[j], src[j] + (ok ? r0 : 0), ok ? 16 : 0);
+  }
+};
 
 struct JacArgs {
   double* X;
@@ -148,11 +160,12 @@ __global__ void __launch_bounds__(JT) jacobi_gram_kernel(JacArgs a) {
 #pragma unroll
   for (int j = 0; j < TPW; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int nch = (int)cdiv_dev(re - rb, CH);
-  if (nch > 0) load_chunk<JB>(buf[0], a.X, a.ld, rb, re, bx, by);
+  const ChunkLoader<JB> ldr(a.X, a.ld, bx, by);
+  if (nch > 0) ldr.load(buf[0], rb, re);
   cp_async_commit();
   for (int i = 0; i < nch; ++i) {
     if (i + 1 < nch)
-      load_chunk<JB>(buf[(i + 1) & 1], a.X, a.ld, rb + (int64_t)(i + 1) * CH, re, bx, by);
+      ldr.load(buf[(i + 1) & 1], rb + (int64_t)(i + 1) * CH, re);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
@@ -420,8 +433,9 @@ __global__ void __launch_bounds__(JT, 2) jacobi_apply_kernel(JacArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
   const int nch = (int)cdiv_dev(re - rb, CH);
+  const ChunkLoader<JB> ldr(M, a.ld, bx, by);
   for (int s = 0; s < NBUF - 1; ++s) {
-    if (s < nch) load_chunk<JB>(asm_ + s * P2 * LDR, M, a.ld, rb + (int64_t)s * CH, re, bx, by);
+    if (s < nch) ldr.load(asm_ + s * P2 * LDR, rb + (int64_t)s * CH, re);
     cp_async_commit();
   }
   const int ct0 = (warp % (NT / CTW)) * CTW, rt0 = (warp / (NT / CTW)) * RTW;
@@ -442,8 +456,7 @@ __global__ void __launch_bounds__(JT, 2) jacobi_apply_kernel(JacArgs a) {
     cp_async_wait<NBUF - 2>();
     __syncthreads();   // chunk i landed; every warp is done with chunk i-1
     if (i + NBUF - 1 < nch)
-      load_chunk<JB>(asm_ + ((i + NBUF - 1) % NBUF) * P2 * LDR, M, a.ld,
-                     rb + (int64_t)(i + NBUF - 1) * CH, re, bx, by);
+      ldr.load(asm_ + ((i + NBUF - 1) % NBUF) * P2 * LDR, rb + (int64_t)(i + NBUF - 1) * CH, re);
     cp_async_commit();
     const double* b = asm_ + (i % NBUF) * P2 * LDR;
     double o[RTW][CTW][2];
