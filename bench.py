@@ -20,6 +20,7 @@ box's cores) and the end-to-end number through the public API.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -100,7 +101,10 @@ def host_cores():
 # ---------------------------------------------------------------------------
 
 class Clocks:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi sampler (200 ms).  It is started before the warm-up (its
+    start-up would otherwise land inside the first timed step) and only the
+    samples stamped inside [start(), stop()] — the timed region — count."""
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -108,6 +112,13 @@ class Clocks:
         self.index = index
         self.proc = None
         self.path = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        self.t0 = datetime.datetime.now()
+
+    def stop(self):
+        self.t1 = datetime.datetime.now()
 
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -140,10 +151,14 @@ class Clocks:
                 if len(f) < 9:
                     continue
                 try:
-                    sm.append(float(f[1]))
-                    mx = float(f[2])
+                    ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f")
+                    if (self.t0 and ts < self.t0) or (self.t1 and ts > self.t1):
+                        continue
+                    clk, cmax = float(f[1]), float(f[2])
                 except ValueError:
                     continue
+                sm.append(clk)
+                mx = cmax
                 for nm, val in zip(names, f[5:9]):
                     if val.lower() == "active":
                         reasons.add(nm)
@@ -243,14 +258,17 @@ def run_b200(args, rank, world, local_rank):
         u, s, v = tnrsvd_prepared(am, o, kw["k_target"], kw["q"], kw["round_tol"])
         return s
 
-    for _ in range(args.warmup):
+    clk = Clocks(local_rank).__enter__()   # sampler up before the warm-up
+    for _ in range(args.warmup):   # same loop body as the timed one (lazy-loaded fill kernel)
+        flush.zero_()
         step()
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     l0 = _lib.launch_count()
     stream = torch.cuda.current_stream()
-    with Clocks(local_rank) as clk:
+    try:
+        clk.start()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         e0.record(stream)
@@ -260,6 +278,9 @@ def run_b200(args, rank, world, local_rank):
             marks[i].record(stream)
         e1.record(stream)
         e1.synchronize()
+        clk.stop()
+    finally:
+        clk.__exit__(None, None, None)
     step_ms = [e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i])
                                              for i in range(1, args.steps)]
     print("[bench] c2 device ms per step:", " ".join(f"{x:.1f}" for x in step_ms), file=sys.stderr)

@@ -608,7 +608,12 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   const int nb = (int)(kp / JB), npairs = nb / 2;
   const double eps = 2.220446049250313e-16;
   const double tol = 8.0 * eps * sqrt((double)std::max<int64_t>(k, 1));
-  int splits = (int)std::min<int64_t>(std::max<int64_t>(1, cdiv(592, npairs)), cdiv(kp, CH));
+  // row splits: npairs * splits <= 592 = one wave of the gram kernel (4 CTAs
+  // per SM) and two waves of the apply kernel (2 per SM); rounding up would
+  // leave a nearly empty tail wave
+  static const int wave =
+      std::getenv("MPO_B200_JWAVE") ? std::atoi(std::getenv("MPO_B200_JWAVE")) : 592;
+  int splits = (int)std::min<int64_t>(std::max<int64_t>(1, wave / npairs), cdiv(kp, CH));
   int64_t rps = cdiv(cdiv(kp, splits), CH) * CH;
   splits = (int)cdiv(kp, rps);
   DBuf<double> gpart((size_t)npairs * splits * P2 * P2, st), J((size_t)npairs * P2 * P2, st);
