@@ -250,6 +250,10 @@ def run_b200(args, rank, world, local_rank):
         return float(t.item())
 
     peak = fp64_peak_tflops(torch)
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+    except (OSError, ValueError):
+        traffic = {}
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
     am, o, kk = prepare(a_host, kw["k_target"], kw["oversample"], kw["seed"])
@@ -328,7 +332,11 @@ def run_b200(args, rank, world, local_rank):
     step_ms = per_step * 1e3
     roofline = {
         "bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": achieved / peak if peak else None, "traffic": None,
+        "frac": achieved / peak if peak else None, "traffic": traffic.get("dram_bytes_per_launch"),
+        "traffic_note": ("dram read+write bytes of one k=4096 launch from the committed ncu "
+                         f"--set full capture ({traffic.get('source')}); algorithmic bytes of "
+                         f"that launch {traffic.get('algorithmic_bytes_per_launch')}")
+        if traffic else None,
         "peak_source": "measured in this run: cuBLAS DGEMM 8192^3 (torch.matmul float64); "
                        "MEASURED_PEAKS.json has no FP64 figure",
         "avg_launch_us": 1e3 * ms_d / max(n_d, 1), "launches_per_step": n_d,
