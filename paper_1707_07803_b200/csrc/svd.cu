@@ -218,8 +218,10 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
   // s_blk lists them, off-diagonal (u < v) first, diagonal last.
   constexpr int NBLK = NPR * (NPR + 1) / 2;
   __shared__ unsigned char s_blk[NBLK][2];
-  __shared__ double rc[NPR], rs[NPR], rdp[NPR], rdq[NPR];
-  __shared__ int rflag[NPR];
+  // rotations double-buffered by round parity: J's update for round r-1
+  // runs (warps 1..) while warp 0 computes round r's rotations
+  __shared__ double rc[2][NPR], rs[2][NPR], rdp[NPR], rdq[NPR];
+  __shared__ int rflag[2][NPR];
   __shared__ int s_skip;
   const int t = threadIdx.x, pair = blockIdx.x, lane = t & 31, warp = t >> 5;
   {
@@ -296,10 +298,26 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     }
   }
   __syncthreads();
+  // J's columns p, q rotated by round rr's rotations (warps jw0.., strided)
+  auto j_update = [&](int rr, int jt, int jn) {
+    const int par = rr & 1;
+    for (int idx = jt; idx < P2 * NPR; idx += jn) {
+      const int w = idx / P2, row = idx % P2;
+      if (!rflag[par][w]) continue;
+      const int p = s_pq[rr][w][0], q = s_pq[rr][w][1];
+      const double c = rc[par][w], s = rs[par][w];
+      const double jp = J[row * GLD + p], jq = J[row * GLD + q];
+      J[row * GLD + p] = c * jp - s * jq;
+      J[row * GLD + q] = s * jp + c * jq;
+    }
+  };
   for (int sweep = 0; sweep < a.inner; ++sweep) {
     int any = 0;
     for (int r = 0; r < P2 - 1; ++r) {
-      if (t < NPR) {
+      const int par = r & 1;
+      if (warp > 0) {
+        if (r > 0) j_update(r - 1, t - 32, ET - 32);
+      } else if (t < NPR) {
         const int p = s_pq[r][t][0], q = s_pq[r][t][1];
         const double gpp = G[p * GLD + p], gqq = G[q * GLD + q], gpq = G[p * GLD + q];
         const double pq = gpp * gqq;
@@ -330,15 +348,17 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
           c *= f;
           s *= f;
         }
-        rc[t] = c; rs[t] = s; rflag[t] = rot;
+        rc[par][t] = c; rs[par][t] = s; rflag[par][t] = rot;
         rdp[t] = fma(c * c, gpp, fma(-2.0 * c * s, gpq, s * s * gqq));
         rdq[t] = fma(s * s, gpp, fma(2.0 * c * s, gpq, c * c * gqq));
         any |= rot;
       }
       __syncthreads();
+      const int* rf = rflag[par];
+      const double *rcp = rc[par], *rsp = rs[par];
       for (int idx = t; idx < NBLK; idx += ET) {
         const int u = s_blk[idx][0], v = s_blk[idx][1];
-        if (!(rflag[u] | rflag[v])) continue;
+        if (!(rf[u] | rf[v])) continue;
         const int pu = s_pq[r][u][0], qu = s_pq[r][u][1];
         if (u == v) {
           G[pu * GLD + pu] = rdp[u];
@@ -347,7 +367,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
           continue;
         }
         const int pv = s_pq[r][v][0], qv = s_pq[r][v][1];
-        const double cu = rc[u], su = rs[u], cv = rc[v], sv = rs[v];
+        const double cu = rcp[u], su = rsp[u], cv = rcp[v], sv = rsp[v];
         // entry (a, b) of the symmetric G lives at min(a,b)*GLD + max(a,b)
         const int a00 = min(pu, pv) * GLD + max(pu, pv), a01 = min(pu, qv) * GLD + max(pu, qv);
         const int a10 = min(qu, pv) * GLD + max(qu, pv), a11 = min(qu, qv) * GLD + max(qu, qv);
@@ -359,18 +379,9 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
         G[a10] = su * x00 + cu * x10;
         G[a11] = su * x01 + cu * x11;
       }
-#pragma unroll
-      for (int h = 0; h < P2 * NPR / ET; ++h) {
-        const int idx = t + h * ET, w = idx / P2, row = idx % P2;
-        if (!rflag[w]) continue;
-        const int p = s_pq[r][w][0], q = s_pq[r][w][1];
-        const double c = rc[w], s = rs[w];
-        const double jp = J[row * GLD + p], jq = J[row * GLD + q];
-        J[row * GLD + p] = c * jp - s * jq;
-        J[row * GLD + q] = s * jp + c * jq;
-      }
       __syncthreads();
     }
+    j_update(P2 - 2, t, ET);   // the last round's J update
     if (!__syncthreads_or(any)) break;
   }
   // re-orthogonalise J: two Newton-Schulz steps J <- J - J (J^T J - I) / 2
