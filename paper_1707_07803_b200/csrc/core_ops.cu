@@ -2,6 +2,8 @@
 // product (rsvd.py:62-79), F-order permutations (the reshape/transpose
 // bookkeeping of rsvd.py:97, :159-160, :192), copies, scaling and the
 // deterministic Frobenius norm of rsvd.py:123.
+#include <deque>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -274,4 +276,20 @@ void core0_finish(cudaStream_t st, const double* in, int64_t I1, int64_t K, int6
   CK_LAUNCH();
   note_launch();
 }
+
+SideStream& side_stream(cudaStream_t main) {
+  thread_local std::deque<SideStream> cache;   // deque: stable references
+  for (auto& x : cache)
+    if (x.main == main) return x;
+  SideStream x;
+  x.main = main;
+  CK(cudaStreamCreateWithFlags(&x.sv, cudaStreamNonBlocking));
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CK(cudaStreamCreateWithPriority(&x.hp, cudaStreamNonBlocking, hi));
+  for (auto& e : x.e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cache.push_back(x);
+  return cache.back();
+}
+
 }  // namespace mpob

@@ -86,4 +86,14 @@ void place_block(cudaStream_t st, const double* in, int64_t Ri, int64_t M, int64
 // out[i, l, r] = in[i, l, r] * sign[l] for l < kt (tnrsvd finishing, rsvd.py:251-257)
 void core0_finish(cudaStream_t st, const double* in, int64_t I1, int64_t K, int64_t R2,
                   int64_t kt, const double* sign_dev, double* out);
+
+// A second (non-blocking) stream and eight events, created once per (host
+// thread, main stream): lets one library call overlap independent work.
+// Events 0-3 belong to the Jacobi sweeps (svd.cu), 4-7 to the QR (qr.cu).
+struct SideStream {
+  cudaStream_t main = nullptr, sv = nullptr;
+  cudaStream_t hp = nullptr;   // highest-priority stream (latency-critical chains)
+  cudaEvent_t e[8] = {};
+};
+SideStream& side_stream(cudaStream_t main);
 }  // namespace mpob

@@ -11,6 +11,7 @@
 // (dorgqr) are DMMA GEMMs (gemm.cu).  Householder convention as dlarfg:
 // beta = -sign(alpha) * ||x||, tau = (beta - alpha) / beta.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -498,9 +499,28 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
       vtv((size_t)gmax * QR_NB * QR_NB, st), alpha(1, st);
   DBuf<double> Tp((size_t)QR_NB * QR_NB, st), S((size_t)NBO * NBO, st), tmp((size_t)NBO * QR_NB, st);
   DBuf<double> W, W2;
+  // look-ahead (see the trailing update below) for matrices with > 2 outer blocks
+  static const bool lookahead = std::getenv("MPO_B200_QR_LOOKAHEAD")
+                                    ? std::atoi(std::getenv("MPO_B200_QR_LOOKAHEAD")) != 0
+                                    : true;
+  const bool la = lookahead && nob > 2 && n > 2 * NBO;
+  SideStream* sd = la ? &side_stream(st) : nullptr;
+  cudaEvent_t ev_panel = la ? sd->e[4] : nullptr, ev_far = la ? sd->e[5] : nullptr;
+  // the panel chain (panels, in-block updates, near updates) runs on the
+  // highest-priority stream so its small launches are scheduled ahead of
+  // the far updates' CTAs
+  cudaStream_t ps = la ? sd->hp : st;
   auto ensure = [&](int64_t sz) {
-    if ((int64_t)W.size() < sz) { W.alloc((size_t)sz, st); W2.alloc((size_t)sz, st); }
+    if ((int64_t)W.size() < sz) { W.alloc((size_t)sz, ps); W2.alloc((size_t)sz, ps); }
   };
+  DBuf<double> Ws, Ws2;
+  if (la) {
+    CK(cudaEventRecord(ev_panel, st));              // A, V, T initialised
+    CK(cudaStreamWaitEvent(sd->sv, ev_panel, 0));
+    CK(cudaStreamWaitEvent(ps, ev_panel, 0));
+    Ws.alloc((size_t)NBO * n, sd->sv);
+    Ws2.alloc((size_t)NBO * n, sd->sv);
+  }
   for (int64_t b = 0; b < nob; ++b) {
     const int64_t j0 = b * NBO, wo = wos[b], mp = m - j0;
     double* Vo = V.get() + voff[b];
@@ -508,15 +528,15 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
     for (int64_t i0 = 0, wi = 0; i0 < wo; i0 += wi) {
       const int64_t jj = j0 + i0, mpi = m - jj;
       wi = std::min<int64_t>(panel_width(mpi, QR_NB), wo - i0);
-      factor_panel(st, A + jj + jj * lda, lda, mpi, wi, Vo + i0 + i0 * mp, mp, Tp.get(),
+      factor_panel(ps, A + jj + jj * lda, lda, mpi, wi, Vo + i0 + i0 * mp, mp, Tp.get(),
                    tau.get() + jj, part.get(), wpart.get(), vtv.get(), alpha.get());
       // place the panel's T on the diagonal of the outer T
-      copy_matrix(st, wi, wi, Tp.get(), wi, To + i0 + i0 * wo, wo);
+      copy_matrix(ps, wi, wi, Tp.get(), wi, To + i0 + i0 * wo, wo);
       if (i0 > 0) {
         // To[0:i0, i0:i0+wi] = -To[0:i0, 0:i0] (V[:, 0:i0]^T V[:, i0:i0+wi]) Tp
-        dgemm(st, true, false, i0, wi, mp, 1.0, Vo, mp, Vo + i0 * mp, mp, 0.0, S.get(), i0);
-        dgemm(st, false, false, i0, wi, i0, 1.0, To, wo, S.get(), i0, 0.0, tmp.get(), i0);
-        dgemm(st, false, false, i0, wi, wi, -1.0, tmp.get(), i0, Tp.get(), wi, 0.0,
+        dgemm(ps, true, false, i0, wi, mp, 1.0, Vo, mp, Vo + i0 * mp, mp, 0.0, S.get(), i0);
+        dgemm(ps, false, false, i0, wi, i0, 1.0, To, wo, S.get(), i0, 0.0, tmp.get(), i0);
+        dgemm(ps, false, false, i0, wi, wi, -1.0, tmp.get(), i0, Tp.get(), wi, 0.0,
               To + i0 * wo, wo);
       }
       // update the rest of this outer block with the panel's reflectors
@@ -525,21 +545,45 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
         double* Ar = A + jj + (jj + wi) * lda;
         const double* Vi = Vo + i0 + i0 * mp;
         ensure(wi * rem);
-        dgemm(st, true, false, wi, rem, mpi, 1.0, Vi, mp, Ar, lda, 0.0, W.get(), wi);
-        dgemm(st, true, false, wi, rem, wi, 1.0, Tp.get(), wi, W.get(), wi, 0.0, W2.get(), wi);
-        dgemm(st, false, false, mpi, rem, wi, -1.0, Vi, mp, W2.get(), wi, 1.0, Ar, lda);
+        dgemm(ps, true, false, wi, rem, mpi, 1.0, Vi, mp, Ar, lda, 0.0, W.get(), wi);
+        dgemm(ps, true, false, wi, rem, wi, 1.0, Tp.get(), wi, W.get(), wi, 0.0, W2.get(), wi);
+        dgemm(ps, false, false, mpi, rem, wi, -1.0, Vi, mp, W2.get(), wi, 1.0, Ar, lda);
       }
     }
     // trailing update of columns j0+wo .. n-1 with the outer block:
-    // A -= V T^T (V^T A)
+    // A -= V T^T (V^T A).  With look-ahead, only the next outer block's
+    // columns ("near") are updated here; the rest ("far") go to the side
+    // stream and overlap the next block's latency-bound panels (<= 16 SMs).
+    // Main waits for far(b-1) before near(b): the near columns were part of
+    // far(b-1)'s range.
     const int64_t nt = n - (j0 + wo);
     if (nt > 0) {
+      const int64_t near = la ? std::min<int64_t>(nt, NBO) : nt, far = nt - near;
       double* At = A + j0 + (j0 + wo) * lda;
-      ensure(wo * nt);
-      dgemm(st, true, false, wo, nt, mp, 1.0, Vo, mp, At, lda, 0.0, W.get(), wo);
-      dgemm(st, true, false, wo, nt, wo, 1.0, To, wo, W.get(), wo, 0.0, W2.get(), wo);
-      dgemm(st, false, false, mp, nt, wo, -1.0, Vo, mp, W2.get(), wo, 1.0, At, lda);
+      if (la) {
+        CK(cudaEventRecord(ev_panel, ps));   // block b's V, T are ready
+        if (b > 0) CK(cudaStreamWaitEvent(ps, ev_far, 0));
+      }
+      ensure(wo * near);
+      dgemm(ps, true, false, wo, near, mp, 1.0, Vo, mp, At, lda, 0.0, W.get(), wo);
+      dgemm(ps, true, false, wo, near, wo, 1.0, To, wo, W.get(), wo, 0.0, W2.get(), wo);
+      dgemm(ps, false, false, mp, near, wo, -1.0, Vo, mp, W2.get(), wo, 1.0, At, lda);
+      if (far > 0) {
+        cudaStream_t sv = sd->sv;
+        double* Af = At + near * lda;
+        CK(cudaStreamWaitEvent(sv, ev_panel, 0));
+        dgemm(sv, true, false, wo, far, mp, 1.0, Vo, mp, Af, lda, 0.0, Ws.get(), wo);
+        dgemm(sv, true, false, wo, far, wo, 1.0, To, wo, Ws.get(), wo, 0.0, Ws2.get(), wo);
+        dgemm(sv, false, false, mp, far, wo, -1.0, Vo, mp, Ws2.get(), wo, 1.0, Af, lda);
+        CK(cudaEventRecord(ev_far, sv));
+      }
     }
+  }
+  if (la) {   // main continues after the last far and the last panel-chain work
+    CK(cudaStreamWaitEvent(st, ev_far, 0));
+    CK(cudaEventRecord(ev_panel, ps));
+    CK(cudaStreamWaitEvent(st, ev_panel, 0));
+    ps = st;   // workspace (re)allocations below are ordered on the main stream
   }
   if (R) {
     extract_r_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(cdiv(k * n, 256), 2368)), 256,

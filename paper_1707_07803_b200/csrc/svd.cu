@@ -676,19 +676,7 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   cudaEvent_t evE[2] = {nullptr, nullptr}, evV[2] = {nullptr, nullptr};
   const bool overlap = !prof && npairs >= 16;   // large problems only
   if (overlap) {
-    // side stream + events cached per (host thread, main stream)
-    struct Side { cudaStream_t main = nullptr, sv = nullptr; cudaEvent_t e[4]; };
-    thread_local std::vector<Side> sides;
-    Side* sd = nullptr;
-    for (auto& x : sides) if (x.main == st) sd = &x;
-    if (!sd) {
-      Side x;
-      x.main = st;
-      CK(cudaStreamCreateWithFlags(&x.sv, cudaStreamNonBlocking));
-      for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&x.e[i], cudaEventDisableTiming));
-      sides.push_back(x);
-      sd = &sides.back();
-    }
+    SideStream* sd = &side_stream(st);   // cached per (host thread, main stream)
     sv = sd->sv;
     evE[0] = sd->e[0]; evE[1] = sd->e[1]; evV[0] = sd->e[2]; evV[1] = sd->e[3];
     for (int i = 0; i < 2; ++i) CK(cudaEventRecord(evV[i], st));
