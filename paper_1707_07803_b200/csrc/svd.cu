@@ -132,6 +132,7 @@ struct JacArgs {
   int ns_steps;    // Newton-Schulz re-orthogonalisation steps on J
   int* skiplog;    // profiling only: per (round, pair) skip flags, or null
   int which;       // apply: 0 = X, 1 = V
+  int cross;       // eig: rotate only the cross-block pairs (NPR inner rounds)
 };
 
 template <int JB>
@@ -280,9 +281,15 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
   // the angle is accurate to ~1e-7 relative, which only affects how much of
   // |gpq| one rotation removes, never the orthogonality of J.  Fresh FP64
   // Grams of the outer rounds decide convergence.
-  for (int idx = t; idx < (P2 - 1) * NPR; idx += ET) {
+  // inner schedule: the full cyclic sweep (circle method, P2-1 rounds), or
+  // with a.cross only the JB x JB cross-block pairs (JB rounds of
+  // (i, JB + (i + r) mod JB)); the blocks' internal pairs were orthogonalised
+  // when the sweep first met them (round 0 uses the full schedule)
+  const int nrounds = a.cross ? NPR : P2 - 1;
+  for (int idx = t; idx < nrounds * NPR; idx += ET) {
     int r = idx / NPR, i = idx % NPR, p, q;
-    pair_of_round(P2, r, i, p, q);
+    if (a.cross) { p = i; q = NPR + (i + r) % NPR; }
+    else pair_of_round(P2, r, i, p, q);
     s_pq[r][i][0] = (unsigned char)min(p, q);
     s_pq[r][i][1] = (unsigned char)max(p, q);
   }
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
   };
   for (int sweep = 0; sweep < a.inner; ++sweep) {
     int any = 0;
-    for (int r = 0; r < P2 - 1; ++r) {
+    for (int r = 0; r < nrounds; ++r) {
       const int par = r & 1;
       if (warp > 0) {
         if (r > 0) j_update(r - 1, t - 32, ET - 32);
@@ -381,7 +388,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
       }
       __syncthreads();
     }
-    j_update(P2 - 2, t, ET);   // the last round's J update
+    j_update(nrounds - 1, t, ET);   // the last round's J update
     if (!__syncthreads_or(any)) break;
   }
   // re-orthogonalise J: two Newton-Schulz steps J <- J - J (J^T J - I) / 2
@@ -634,6 +641,10 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   // one step suffices: every rotation is orthogonal to O(eps) (FP64
   // renormalised), so J's defect after one inner sweep is ~P2 eps and one
   // quadratic step takes it to rounding level
+  // MPO_B200_CROSS_FROM=s: from sweep s on, rounds after a sweep's first
+  // use cross-block-only inner sweeps (-1: never)
+  static const int cross_from =
+      std::getenv("MPO_B200_CROSS_FROM") ? std::atoi(std::getenv("MPO_B200_CROSS_FROM")) : 0;
   static const int ns_steps =
       std::getenv("MPO_B200_NS") ? std::atoi(std::getenv("MPO_B200_NS")) : 1;
   // J and skip flags are double-buffered by round parity: the V updates of
@@ -737,6 +748,7 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
     for (int r = 0; r < nb - 1; ++r, ++rr) {
       const int par = (int)(rr & 1);
       a.round = r;
+      a.cross = cross_from >= 0 && sweep >= cross_from && r > 0;
       a.J = Jb[par];
       a.skip = Sb[par];
       if (prof) CK(cudaEventRecord(ev[4 * r], st));
