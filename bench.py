@@ -295,7 +295,13 @@ def run_b200(args, rank, world, local_rank):
     per_step = secs / args.steps
     value = world * flops / per_step / 1e12
 
-    # end to end through the public API: host Mpo in, host Mpo out
+    # end to end through the public API: host Mpo in, host Mpo out.  Same
+    # warm-up rule as above (the first calls populate the pinned host pool
+    # the downloads land in)
+    for _ in range(args.warmup):
+        flush.zero_()
+        lr = m.tnrsvd(a_host, **kw)
+    del lr
     barrier()
     torch.cuda.synchronize()
     h2d = sum(c.nbytes for c in a_host.cores)

@@ -193,7 +193,7 @@ class DeviceMpo:
 
     def core(self, k: int) -> np.ndarray:
         shp = self.shapes[k]
-        out = np.empty(shp, dtype=np.float64, order="F")
+        out = _host_buffer(shp)
         _lib.call("mpo_dev_copy_core", self.ctx, self.handle, k, C.c_void_p(out.ctypes.data), 1)
         return out
 
@@ -215,6 +215,22 @@ class DeviceMpo:
 
     def __repr__(self):
         return f"DeviceMpo(d={self.num_cores}, ranks={list(self.ranks)})"
+
+
+def _host_buffer(shape) -> np.ndarray:
+    """F-ordered float64 host array for a download.  Backed by page-locked
+    memory from torch's caching host allocator when CUDA is up (the D2H
+    copy then runs at full link speed and the pages are recycled across
+    calls, not faulted in afresh); plain numpy otherwise."""
+    n = prod(shape)
+    try:
+        import torch  # plumbing only: the pinned host allocator
+        if torch.cuda.is_available() and n >= (1 << 16):
+            t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            return t.numpy().reshape(shape, order="F")
+    except ImportError:  # pragma: no cover
+        pass
+    return np.empty(shape, dtype=np.float64, order="F")
 
 
 def _wrap(ctx, handle) -> DeviceMpo:
