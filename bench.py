@@ -475,6 +475,11 @@ def bench_conversion(args, torch, dist, rank, world, dev, barrier, max_over_rank
     # end to end: host COO in, host (i1, j1, ti, values, uniq) out
     import paper_1707_07803_b200 as m
     rs, cs_, vs = r[lo:hi], c[lo:hi], v[lo:hi]
+    for _ in range(args.warmup):   # populates the pinned host pool of the downloads
+        rr = m.convert_structure(rs, cs_, vs, plan)
+        arrs = rr.arrays()
+        rr.free()
+    del arrs
     t0 = time.perf_counter()
     for _ in range(args.steps):
         rr = m.convert_structure(rs, cs_, vs, plan)

@@ -129,6 +129,23 @@ def launch_count() -> int:
     return int(load().mpo_b200_launch_count())
 
 
+def host_empty(shape, dtype=np.float64, order="C"):
+    """Host array for a download.  Backed by page-locked memory from torch's
+    caching host allocator when CUDA is up (the D2H copy runs at full link
+    speed and the pages are recycled across calls instead of faulted in
+    afresh); plain numpy for small arrays or without CUDA."""
+    shape = tuple(int(s) for s in (shape if isinstance(shape, (tuple, list)) else (shape,)))
+    n = int(np.prod(shape)) if shape else 1
+    try:
+        import torch  # plumbing only: the pinned host allocator
+        if n >= (1 << 16) and torch.cuda.is_available():
+            tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64}[np.dtype(dtype)]
+            return torch.empty(n, dtype=tdt, pin_memory=True).numpy().reshape(shape, order=order)
+    except (ImportError, KeyError):  # pragma: no cover
+        pass
+    return np.empty(shape, dtype=dtype, order=order)
+
+
 def as_i64(a):
     return np.ascontiguousarray(a, dtype=np.int64)
 

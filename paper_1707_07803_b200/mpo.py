@@ -218,19 +218,8 @@ class DeviceMpo:
 
 
 def _host_buffer(shape) -> np.ndarray:
-    """F-ordered float64 host array for a download.  Backed by page-locked
-    memory from torch's caching host allocator when CUDA is up (the D2H
-    copy then runs at full link speed and the pages are recycled across
-    calls, not faulted in afresh); plain numpy otherwise."""
-    n = prod(shape)
-    try:
-        import torch  # plumbing only: the pinned host allocator
-        if torch.cuda.is_available() and n >= (1 << 16):
-            t = torch.empty(n, dtype=torch.float64, pin_memory=True)
-            return t.numpy().reshape(shape, order="F")
-    except ImportError:  # pragma: no cover
-        pass
-    return np.empty(shape, dtype=np.float64, order="F")
+    """F-ordered float64 (pinned when CUDA is up) host array for a download."""
+    return _lib.host_empty(shape, np.float64, order="F")
 
 
 def _wrap(ctx, handle) -> DeviceMpo:

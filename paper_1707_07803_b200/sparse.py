@@ -97,15 +97,16 @@ class ConversionResult:
     def arrays(self):
         """(i1, j1, ti, values, uniq) as host arrays."""
         n, r = self.nkept, self.rank
-        i1 = np.empty(n, np.int64); j1 = np.empty(n, np.int64); ti = np.empty(n, np.int64)
-        v = np.empty(n, np.float64); u = np.empty(r, np.int64)
+        i1, j1, ti = (_lib.host_empty(n, np.int64) for _ in range(3))
+        v = _lib.host_empty(n, np.float64)
+        u = _lib.host_empty(r, np.int64)
         _lib.call("mpo_conv_copy", self.ctx, self.handle, _lib.ptr(i1), _lib.ptr(j1),
                   _lib.ptr(ti), _lib.ptr(v), _lib.ptr(u), 1)
         return i1, j1, ti, v, u
 
     def level(self, k: int):
         """Block digits (row, col) of core k >= 1 (sparse.py:249-250)."""
-        rd = np.empty(self.rank, np.int64); cd = np.empty(self.rank, np.int64)
+        rd = _lib.host_empty(self.rank, np.int64); cd = _lib.host_empty(self.rank, np.int64)
         _lib.call("mpo_conv_level", self.ctx, self.handle, int(k), _lib.ptr(rd), _lib.ptr(cd), 1)
         return rd, cd
 
