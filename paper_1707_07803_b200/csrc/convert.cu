@@ -155,10 +155,18 @@ __global__ void radix_hist(const uint64_t* __restrict__ key, int64_t n, int shif
   for (int d = threadIdx.x; d < WARPS * RADIX; d += CT) (&wh[0][0])[d] = 0;
   __syncthreads();
   const int64_t wbase = blockIdx.x * (int64_t)TILE + warp * WITEMS;
+  // all loads in flight before the ranking loop (its __syncwarp()s are
+  // memory fences that would otherwise expose one load latency per item)
+  unsigned digs[ITEMS];
+#pragma unroll
   for (int it = 0; it < ITEMS; ++it) {
-    int64_t i = wbase + it * 32 + lane;
-    bool valid = i < n;
-    unsigned dig = valid ? (unsigned)((key[i] >> shift) & (RADIX - 1)) : RADIX;  // RADIX = invalid
+    const int64_t i = wbase + it * 32 + lane;
+    digs[it] = i < n ? (unsigned)((key[i] >> shift) & (RADIX - 1)) : RADIX;  // RADIX = invalid
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const unsigned dig = digs[it];
+    const bool valid = dig < RADIX;
     unsigned peers = __match_any_sync(0xffffffffu, dig);
     int leader = __ffs(peers) - 1;
     if (valid && lane == leader) wh[warp][dig] += __popc(peers);
@@ -200,11 +208,15 @@ __global__ void __launch_bounds__(CT) radix_scatter(const uint64_t* __restrict__
   uint64_t k[ITEMS];
   unsigned pv[ITEMS], rank[ITEMS];
 #pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {
-    int64_t i = wbase + it * 32 + lane;
-    bool valid = i < n;
+  for (int it = 0; it < ITEMS; ++it) {   // all loads first (see radix_hist)
+    const int64_t i = wbase + it * 32 + lane;
+    const bool valid = i < n;
     k[it] = valid ? key[i] : 0;
     pv[it] = valid ? pay[i] : 0;
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const bool valid = wbase + it * 32 + lane < n;
     unsigned dig = valid ? (unsigned)((k[it] >> shift) & (RADIX - 1)) : RADIX;
     unsigned peers = __match_any_sync(0xffffffffu, dig);
     int leader = __ffs(peers) - 1;
