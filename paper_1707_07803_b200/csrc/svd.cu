@@ -13,8 +13,10 @@
 //   eig   : one CTA per pair sums the partials in a fixed order, tests
 //           convergence, runs one cyclic two-sided Jacobi sweep on the Gram
 //           matrix in shared memory (FP32-seeded, FP64-renormalised
-//           rotations) and re-orthogonalises the accumulated rotation J with
-//           two Newton-Schulz steps on the DMMA pipe;
+//           rotations; after a sweep's first round only the cross-block
+//           pairs) and, in full sweeps, re-orthogonalises the accumulated
+//           rotation J with a Newton-Schulz step on the DMMA pipe (V gets
+//           one step after the last sweep);
 //   apply : (pair, row split, X|V) CTAs stream rows again and multiply by J
 //           on the DMMA pipe, in place.
 // 64-column pairs halve the rounds per sweep (and so the HBM traffic per
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     double sacc[PER];
 #pragma unroll
     for (int e = 0; e < PER; ++e) sacc[e] = 0.0;
+#pragma unroll 4
     for (int sp = 0; sp < a.splits; ++sp) {
       double v[PER];
 #pragma unroll
@@ -397,7 +400,10 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
   constexpr int NW = ET / 32, TPW = K::NT * K::NT / NW;
   double* E = G;
   const int ti = warp % K::NT, tj0 = (warp / K::NT) * TPW;
-  for (int it = 0; it < a.ns_steps; ++it) {
+  // cross-block eigs skip it: their J (1024 rotations, each orthogonal to
+  // FP64 rounding) is orthogonal to ~1e-14 and V is re-orthogonalised once
+  // after the sweeps (jacobi_sweeps)
+  for (int it = 0; it < (a.cross ? 0 : a.ns_steps); ++it) {
     __syncthreads();
     double acc[TPW][2];
     mmP<JB, TPW, true>(J, J, acc, ti, tj0, lane);
@@ -808,6 +814,15 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   if (a.X != X) {   // sorted copies live in the scratch buffers
     CK(cudaMemcpyAsync(X, a.X, sizeof(double) * kp * kp, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(V, a.V, sizeof(double) * kp * kp, cudaMemcpyDeviceToDevice, st));
+  }
+  if (cross_from >= 0 && ns_steps > 0) {
+    // one Newton-Schulz step on V: V <- V - V (V^T V - I) / 2 (the
+    // cross-block eigs accumulate O(eps) defects per round without one)
+    DBuf<double> E((size_t)kp * kp, st), VE((size_t)kp * kp, st);
+    set_identity(st, kp, kp, E.get(), kp);
+    dgemm(st, true, false, kp, kp, kp, 1.0, V, kp, V, kp, -1.0, E.get(), kp);
+    dgemm(st, false, false, kp, kp, kp, 1.0, V, kp, E.get(), kp, 0.0, VE.get(), kp);
+    dgemm_axpy(st, kp * kp, -0.5, VE.get(), V);
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return sweeps;
