@@ -836,7 +836,7 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   // 32-column blocks for large k, 16-column blocks for small k (the inner
   // Jacobi latency dominates small problems)
   static const int64_t jb_split =
-      std::getenv("MPO_B200_JB16_MAXK") ? std::atoll(std::getenv("MPO_B200_JB16_MAXK")) : 512;
+      std::getenv("MPO_B200_JB16_MAXK") ? std::atoll(std::getenv("MPO_B200_JB16_MAXK")) : 1024;
   const int jbw = k <= jb_split ? 16 : 32;
   const int64_t kp = cdiv(k, 2 * jbw) * 2 * jbw;
   static const bool trace = std::getenv("MPO_B200_TRACE") != nullptr;
