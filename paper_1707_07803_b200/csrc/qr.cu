@@ -51,24 +51,27 @@ __device__ __forceinline__ double warp_sum(double v) {
 // the i < j entries in parallel: T(0:j, j) = -tau_j T(0:j,0:j) S(0:j, j),
 // S = V^T V (strict upper part used).  Writes T (w x w, column-major) and
 // tau to global memory.  Called by all threads of one CTA.
+//
+// Formulated column-parallel: for true reflectors (tau_j = 2 / v_j^T v_j)
+// T^{-1} = diag(1/tau) + striu(V^T V), so column i of T is the
+// back-substitution x_i = tau_i, x_r = -tau_r sum_{l=r+1..i} S(r,l) x_l
+// (r = i-1 .. 0) -- one thread per column, no barriers between steps; a
+// tau_r = 0 (H_r = I) zeroes row and column r exactly as the recurrence does.
 __device__ void build_t_factor(const double* S, double* sT, const double* tau_in, int w,
                                double* T, double* tau_out) {
   const int t = threadIdx.x;
-  for (int j = 0; j < w; ++j) {
-    const double tj = tau_in[j];
-    if (t < w) {
-      double v;
-      if (t < j) {
-        double acc = 0.0;
-        for (int l = t; l < j; ++l) acc = fma(sT[t + l * w], S[l + j * w], acc);
-        v = -tj * acc;
-      } else {
-        v = (t == j) ? tj : 0.0;
-      }
-      sT[t + j * w] = v;
+  if (t < w) {
+    const int i = t;
+    double* x = sT + i * w;
+    for (int r = i + 1; r < w; ++r) x[r] = 0.0;
+    x[i] = tau_in[i];
+    for (int r = i - 1; r >= 0; --r) {
+      double acc = 0.0;
+      for (int l = r + 1; l <= i; ++l) acc = fma(S[r + l * w], x[l], acc);
+      x[r] = -tau_in[r] * acc;
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int idx = t; idx < w * w; idx += blockDim.x) T[idx] = sT[idx];
   for (int idx = t; idx < w; idx += blockDim.x) tau_out[idx] = tau_in[idx];
 }
@@ -358,7 +361,11 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
     // sum the V^T V partials (fixed rank order) in place, then dlarft
     for (int idx = t; idx < w * w; idx += QR_THREADS) {
       double tot = 0.0;
-      for (int i = 0; i < CS; ++i) tot += cluster.map_shared_rank(s_vtv, i)[idx];
+      double xv[16];   // all remote loads in flight, then the rank-order sum
+#pragma unroll
+      for (int i = 0; i < 16; ++i) xv[i] = i < CS ? cluster.map_shared_rank(s_vtv, i)[idx] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) tot += xv[i];
       chunk[idx] = tot;  // reuse own chunk (already written back)
     }
     __syncthreads();
