@@ -117,27 +117,6 @@ Cores merge_leading(cudaStream_t st, const Cores& m, int count) {
 
 namespace {
 
-// MPO_B200_TRACE=1: per-call device timing of the dense factorizations
-// (synchronises around each call; diagnostics only)
-struct Trace {
-  bool on;
-  cudaStream_t st;
-  const char* what;
-  int64_t m, n;
-  std::chrono::steady_clock::time_point t0;
-  Trace(cudaStream_t s, const char* w, int64_t mm, int64_t nn) : st(s), what(w), m(mm), n(nn) {
-    static const bool env = std::getenv("MPO_B200_TRACE") != nullptr;
-    on = env;
-    if (on) { cudaStreamSynchronize(st); t0 = std::chrono::steady_clock::now(); }
-  }
-  ~Trace() {
-    if (!on) return;
-    cudaStreamSynchronize(st);
-    double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    fprintf(stderr, "[mpo_b200] %s %lldx%lld %.3f ms\n", what, (long long)m, (long long)n, ms);
-  }
-};
-
 // mpo.py:297-304, evaluated on the host from the device singular values
 int64_t truncation_rank(const std::vector<double>& s, double delta, double rel_tol) {
   const int64_t n = (int64_t)s.size();
@@ -183,52 +162,81 @@ void l2r(cudaStream_t st, Cores& cores) {
   }
 }
 
+// rsvd.py:111-136, the truncating half: cores are left-orthonormal (after
+// l2r or orthogonalize_product); delta from the last core's norm (:123)
+void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
+  const size_t d = cores.size();
+  if (d == 1) return;
+  const double delta = tol * device_norm(st, cores.back()) / std::sqrt((double)(d - 1));
+  for (size_t k = d - 1; k >= 1; --k) {
+    Core& c = cores[k];
+    const int64_t R = c.R, N = c.I * c.J * c.S;
+    Core& pv = cores[k - 1];
+    const int64_t Mp = pv.R * pv.I * pv.J;
+    SvdOut o;
+    {
+      Trace tr(st, "svd", R, N);
+      svd_thin(st, R, N, c.p(), R, o, /*noise_floor=*/true);
+    }
+    std::vector<double> s(o.k);
+    CK(cudaMemcpyAsync(s.data(), o.s.get(), sizeof(double) * o.k, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t rr = truncation_rank(s, delta, tol);
+    Core nc = make_core(st, rr, c.I, c.J, c.S);
+    copy_matrix(st, rr, N, o.vh.get(), o.k, nc.p(), rr);
+    Core np_ = make_core(st, pv.R, pv.I, pv.J, rr);
+    dgemm(st, false, false, Mp, rr, R, 1.0, pv.p(), Mp, o.ucarry.get(), R, 0.0, np_.p(), Mp);
+    cores[k] = std::move(nc);
+    cores[k - 1] = std::move(np_);
+  }
+}
+
 // rsvd.py:111-136
 void r2l(cudaStream_t st, Cores& cores, bool has_tol, double tol) {
   const size_t d = cores.size();
   if (d == 1) return;
-  double delta = 0.0;
   if (has_tol) {
-    l2r(st, cores);
-    delta = tol * device_norm(st, cores.back()) / std::sqrt((double)(d - 1));
+    if (tol > 0.0 && fused_sweeps_enabled())
+      cores = orthogonalize_product(st, nullptr, false, nullptr, false, &cores);
+    else
+      l2r(st, cores);
+    truncate_r2l(st, cores, tol);
+    return;
   }
   for (size_t k = d - 1; k >= 1; --k) {
     Core& c = cores[k];
     const int64_t R = c.R, N = c.I * c.J * c.S;
     Core& pv = cores[k - 1];
     const int64_t Mp = pv.R * pv.I * pv.J;
-    if (has_tol) {
-      SvdOut o;
-      {
-        Trace tr(st, "svd", R, N);
-        svd_thin(st, R, N, c.p(), R, o, /*noise_floor=*/true);
-      }
-      std::vector<double> s(o.k);
-      CK(cudaMemcpyAsync(s.data(), o.s.get(), sizeof(double) * o.k, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      const int64_t rr = truncation_rank(s, delta, tol);
-      Core nc = make_core(st, rr, c.I, c.J, c.S);
-      copy_matrix(st, rr, N, o.vh.get(), o.k, nc.p(), rr);
-      Core np_ = make_core(st, pv.R, pv.I, pv.J, rr);
-      dgemm(st, false, false, Mp, rr, R, 1.0, pv.p(), Mp, o.ucarry.get(), R, 0.0, np_.p(), Mp);
-      cores[k] = std::move(nc);
-      cores[k - 1] = std::move(np_);
-    } else {
-      const int64_t kk = std::min(N, R);
-      DBuf<double> At((size_t)(N * R), st), Qt((size_t)(N * kk), st), Rt((size_t)(kk * R), st);
-      int64_t dims[2] = {R, N};
-      int perm[2] = {1, 0};
-      permute(st, c.p(), At.get(), 2, dims, perm);
-      householder_qr(st, N, R, At.get(), N, Qt.get(), N, Rt.get(), kk);
-      Core nc = make_core(st, kk, c.I, c.J, c.S);
-      int64_t d2[2] = {N, kk};
-      permute(st, Qt.get(), nc.p(), 2, d2, perm);
-      Core np_ = make_core(st, pv.R, pv.I, pv.J, kk);
-      dgemm(st, false, true, Mp, kk, R, 1.0, pv.p(), Mp, Rt.get(), kk, 0.0, np_.p(), Mp);
-      cores[k] = std::move(nc);
-      cores[k - 1] = std::move(np_);
-    }
+    const int64_t kk = std::min(N, R);
+    DBuf<double> At((size_t)(N * R), st), Qt((size_t)(N * kk), st), Rt((size_t)(kk * R), st);
+    int64_t dims[2] = {R, N};
+    int perm[2] = {1, 0};
+    permute(st, c.p(), At.get(), 2, dims, perm);
+    householder_qr(st, N, R, At.get(), N, Qt.get(), N, Rt.get(), kk);
+    Core nc = make_core(st, kk, c.I, c.J, c.S);
+    int64_t d2[2] = {N, kk};
+    permute(st, Qt.get(), nc.p(), 2, d2, perm);
+    Core np_ = make_core(st, pv.R, pv.I, pv.J, kk);
+    dgemm(st, false, true, Mp, kk, R, 1.0, pv.p(), Mp, Rt.get(), kk, 0.0, np_.p(), Mp);
+    cores[k] = std::move(nc);
+    cores[k - 1] = std::move(np_);
   }
+}
+
+// The rounded product op(a)·op(b) (rsvd.py:77 then :111-136): fused and
+// rank-bounded for round_tol > 0 (sweep.cu), else materialised like the
+// reference.
+Cores rounded_product(cudaStream_t st, const Cores& a, bool ta, const Cores& b, bool tb,
+                      bool has_tol, double tol) {
+  if (has_tol && tol > 0.0 && fused_sweeps_enabled() && a.size() > 1) {
+    Cores cores = orthogonalize_product(st, &a, ta, &b, tb, nullptr);
+    truncate_r2l(st, cores, tol);
+    return cores;
+  }
+  Cores cores = matmul(st, a, ta, b, tb);
+  r2l(st, cores, has_tol, tol);
+  return cores;
 }
 
 }  // namespace
@@ -272,13 +280,14 @@ Cores add(cudaStream_t st, const Cores& a, const Cores& b) {
 }
 
 // ---- rsvd.py:139-166 --------------------------------------------------------
-Cores qr(cudaStream_t st, const Cores& y, bool has_tol, double tol, DBuf<double>* r_out) {
-  const Core& f = y[0];
-  if (f.I < f.J)
-    throw ValueError("first core has I1 = " + std::to_string(f.I) + " < K = " +
-                     std::to_string(f.J) + "; merge leading cores first");
-  Cores cores = clone(st, y);
-  r2l(st, cores, has_tol, tol);
+namespace {
+void check_qr_input(int64_t I1, int64_t K) {
+  if (I1 < K)
+    throw ValueError("first core has I1 = " + std::to_string(I1) + " < K = " +
+                     std::to_string(K) + "; merge leading cores first");
+}
+// first-core QR of (I1·R2 x K) on the rounded chain (rsvd.py:158-163)
+Cores qr_finish(cudaStream_t st, Cores cores, DBuf<double>* r_out) {
   Core& c0 = cores[0];
   const int64_t I1 = c0.I, K = c0.J, R2 = c0.S;
   DBuf<double> Bt((size_t)(I1 * R2 * K), st), Qt((size_t)(I1 * R2 * K), st), Rt((size_t)(K * K), st);
@@ -291,16 +300,31 @@ Cores qr(cudaStream_t st, const Cores& y, bool has_tol, double tol, DBuf<double>
   if (r_out) *r_out = std::move(Rt);
   return cores;
 }
+}  // namespace
+
+Cores qr(cudaStream_t st, const Cores& y, bool has_tol, double tol, DBuf<double>* r_out) {
+  check_qr_input(y[0].I, y[0].J);
+  Cores cores = clone(st, y);
+  r2l(st, cores, has_tol, tol);
+  return qr_finish(st, std::move(cores), r_out);
+}
+
+// mpo_qr(mpo_matmul(op(a), op(b))) without materialising the product
+Cores qr_of_product(cudaStream_t st, const Cores& a, bool ta, const Cores& b, bool tb,
+                    bool has_tol, double tol) {
+  check_qr_input(ta ? a[0].J : a[0].I, tb ? b[0].I : b[0].J);
+  return qr_finish(st, rounded_product(st, a, ta, b, tb, has_tol, tol), nullptr);
+}
 
 // ---- rsvd.py:169-193 --------------------------------------------------------
-Cores svd(cudaStream_t st, const Cores& b, bool has_tol, double tol, DBuf<double>& w,
-          DBuf<double>& s) {
-  const Core& f = b[0];
-  if (f.J < f.I)
-    throw ValueError("first core has J1 = " + std::to_string(f.J) + " < K = " +
-                     std::to_string(f.I) + "; merge leading cores first");
-  Cores cores = clone(st, b);
-  r2l(st, cores, has_tol, tol);
+namespace {
+void check_svd_input(int64_t K, int64_t J1) {
+  if (J1 < K)
+    throw ValueError("first core has J1 = " + std::to_string(J1) + " < K = " +
+                     std::to_string(K) + "; merge leading cores first");
+}
+// first-core SVD of (K x J1·R2) on the rounded chain (rsvd.py:188-192)
+Cores svd_finish(cudaStream_t st, Cores cores, DBuf<double>& w, DBuf<double>& s) {
   Core& c0 = cores[0];
   const int64_t K = c0.I, N = c0.J * c0.S;
   SvdOut o;
@@ -311,15 +335,24 @@ Cores svd(cudaStream_t st, const Cores& b, bool has_tol, double tol, DBuf<double
   CK(cudaMemcpyAsync(c0.p(), o.vh.get(), sizeof(double) * K * N, cudaMemcpyDeviceToDevice, st));
   return transpose(st, cores);
 }
+}  // namespace
+
+Cores svd(cudaStream_t st, const Cores& b, bool has_tol, double tol, DBuf<double>& w,
+          DBuf<double>& s) {
+  check_svd_input(b[0].I, b[0].J);
+  Cores cores = clone(st, b);
+  r2l(st, cores, has_tol, tol);
+  return svd_finish(st, std::move(cores), w, s);
+}
 
 // ---- rsvd.py:196-214 --------------------------------------------------------
 Cores subspace_iteration(cudaStream_t st, const Cores& a, const Cores& o, int q, bool has_tol,
                          double tol) {
   if (q < 0) throw ValueError("q must be >= 0");
-  Cores qm = qr(st, matmul(st, a, false, o, false), has_tol, tol, nullptr);
+  Cores qm = qr_of_product(st, a, false, o, false, has_tol, tol);
   for (int it = 0; it < q; ++it) {
-    qm = qr(st, matmul(st, a, true, qm, false), has_tol, tol, nullptr);
-    qm = qr(st, matmul(st, a, false, qm, false), has_tol, tol, nullptr);
+    qm = qr_of_product(st, a, true, qm, false, has_tol, tol);
+    qm = qr_of_product(st, a, false, qm, false, has_tol, tol);
   }
   return qm;
 }
@@ -331,9 +364,9 @@ void tnrsvd(cudaStream_t st, const Cores& am, const Cores& o, int k_target, int 
   const int64_t K = o[0].J;
   if (k_target > K) throw ValueError("k_target exceeds the sketch width");
   Cores qm = subspace_iteration(st, am, o, q, has_tol, tol);
-  Cores b = matmul(st, qm, true, am, false);
   DBuf<double> w, s;
-  Cores vt = svd(st, b, has_tol, tol, w, s);
+  check_svd_input(K, am[0].J);
+  Cores vt = svd_finish(st, rounded_product(st, qm, true, am, false, has_tol, tol), w, s);
   // U core 0 = einsum("xikr,kl->xilr", Q1, W): batched over r
   const Core& q0 = qm[0];
   const int64_t I1 = q0.I, R2 = q0.S;

@@ -195,6 +195,12 @@ def big():
     # config-5 TNrSVD instance, oracle-feasible q=0 variant (instance seed 50)
     a = rmpo.random_mpo([2] * 20, [2] * 20, [16] * 19, seed=50)
     cases["c5inst_q0"] = (a, dict(k_target=16, q=0, round_tol=1e-9, oversample=1.5, seed=51))
+    # config-5 recipe (rank 16, q=1) at d=16: the largest d at which the
+    # reference's materialised B = Q^T A cores (12288 x 2 x 16384) still fit
+    # in host memory; exercises the device's fused, rank-bounded sweeps where
+    # the product ranks exceed the bond extents 16-fold
+    a = rmpo.random_mpo([2] * 16, [2] * 16, [16] * 15, seed=50)
+    cases["c5d16_q1"] = (a, dict(k_target=16, q=1, round_tol=1e-9, oversample=1.5, seed=51))
     # config 3 at the oracle-feasible q=0 (q=2 dies with a 1.5 TiB core):
     # cores N(0,1)/8, middle bond (core 5's right rank index k) scaled by 0.5^k
     a = rmpo.random_mpo([4] * 12, [4] * 12, [64] * 11, seed=3)

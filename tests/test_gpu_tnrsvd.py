@@ -180,6 +180,42 @@ def test_c5_instance_q0_full_size():
     assert _ortho_err(lr.u.cores) <= 1e-12 and _ortho_err(lr.v.cores) <= 1e-12
 
 
+def test_c5_recipe_d16_q1():
+    """Config-5 recipe (rank 16, K=16, p=8) at q=1 and d=16, the largest d
+    whose materialised B = Q^T A cores (12288 x 2 x 16384) the reference can
+    hold: the device's fused rank-bounded sweeps (sweep.cu) never form them,
+    yet every output rank equals the reference run and s is within 1e-8
+    (big_c5d16_q1.npz)."""
+    m = _api()
+    z = load_golden("big_c5d16_q1.npz")
+    a = m.random_mpo([2] * 16, [2] * 16, [16] * 15, seed=50)
+    lr = m.tnrsvd(a, 16, q=1, round_tol=1e-9, oversample=1.5, seed=51)
+    assert lr.u.ranks == tuple(z["u_ranks"]) and lr.v.ranks == tuple(z["v_ranks"])
+    np.testing.assert_allclose(lr.s, z["s"], rtol=S_RTOL)
+    assert _ortho_err(lr.u.cores) <= 1e-12 and _ortho_err(lr.v.cores) <= 1e-12
+
+
+def test_c5_instance_q1_full_size():
+    """Config-5 instance exactly as BASELINE.json states it (d=20, q=1): the
+    reference dies materialising a 48 GiB product core (rsvd.py:77), so the
+    check is size-independent: U and V orthonormal, s sorted and positive,
+    ranks within the exact bounds min(left, right extent), deterministic."""
+    m = _api()
+    from paper_1707_07803_b200.workloads import TNRSVD_ARGS, config_mpo
+    a = config_mpo("c5inst")
+    lr = m.tnrsvd(a, **TNRSVD_ARGS["c5inst"])
+    assert np.all(np.diff(lr.s) <= 0) and lr.s[-1] > 0
+    assert _ortho_err(lr.u.cores) <= 1e-11 and _ortho_err(lr.v.cores) <= 1e-11
+    kk = lr.k_oversampled
+    for ranks in (lr.u.ranks, lr.v.ranks):
+        for j in range(1, len(ranks) - 1):
+            left = 32 * kk * 2 ** (j - 1)
+            right = 2 ** (len(ranks) - 1 - j)
+            assert ranks[j] <= min(left, right)
+    lr2 = m.tnrsvd(a, **TNRSVD_ARGS["c5inst"])
+    assert np.array_equal(lr.s, lr2.s)
+
+
 def test_c3_q0_full_size():
     """Config 3 (d=10, 4096x4096 per mode pair, rank 64) at q=0 — the largest
     configuration the reference finishes on CPU here (213 s): singular values

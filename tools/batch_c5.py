@@ -1,6 +1,7 @@
-"""Config-5 batched TNrSVD: 64 independent instances (q=0, oracle-feasible),
-run with T host threads, each on its own CUDA stream (diagnostic)."""
-import sys, time, threading
+"""Config-5 batched TNrSVD: N independent instances (CFG=c5inst_q0 or
+c5inst for q=1), run with T host threads, each on its own CUDA stream
+(diagnostic)."""
+import os, sys, time, threading
 sys.path.insert(0, ".")
 import numpy as np
 import torch
@@ -9,8 +10,9 @@ from paper_1707_07803_b200.rsvd import prepare, tnrsvd_prepared
 from paper_1707_07803_b200.workloads import TNRSVD_ARGS, config_mpo
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 64
-kw = dict(TNRSVD_ARGS["c5inst_q0"])
-inst = [config_mpo("c5inst_q0", i) for i in range(N)]
+CFG = os.environ.get("CFG", "c5inst_q0")
+kw = dict(TNRSVD_ARGS[CFG])
+inst = [config_mpo(CFG, i) for i in range(N)]
 streams = [torch.cuda.Stream() for _ in range(T)]
 prepared = [None] * N
 def prep(i, s):
@@ -31,4 +33,5 @@ for rep in range(2):
     for x in th: x.join()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    print(f"rep {rep}: {dt:.3f} s", flush=True)
 print(f"threads {T} instances {N} seconds {dt:.3f} per-instance {dt/N*1e3:.1f} ms; s0 {out[0][:3]}")
