@@ -45,15 +45,90 @@ __global__ void identity_kernel(int64_t m, int64_t n, double* A, int64_t lda) {
   }
 }
 
+// Permutation of an F-ordered array, after unit axes are dropped and axes
+// that stay adjacent are merged (host side).  A tile is 32 "x" positions
+// (the input-fastest axis, or the first two input axes when the fastest is
+// shorter than 32) by 32 "y" positions (the output-fastest axis, or the
+// first two output axes), staged through shared memory so global reads run
+// along x and global writes along y, both coalesced; the remaining axes are
+// decomposed once per tile, not per element.
+constexpr int TP = 32;
+struct PermAxis2 {
+  int64_t n1, n2;      // extents of the first / second axis of the group
+  int64_t c2;          // positions of the second axis per tile (1 if single)
+  int64_t is1, is2;    // input strides
+  int64_t os1, os2;    // output strides
+  int64_t tiles;
+  bool comp;           // two-axis group
+};
 struct PermArgs {
-  int rank;
-  int64_t odims[6];    // output extents
-  int64_t istride[6];  // input stride of the input axis feeding output axis q
-  int64_t total;
+  PermAxis2 X, Y;
+  int nrest;
+  int64_t rdim[4], ris[4], ros[4];  // remaining axes: extent, in/out strides
+  int64_t ntiles;
 };
 
-__global__ void permute_kernel(const double* __restrict__ in, double* __restrict__ out,
-                               PermArgs a) {
+struct PermIdx {
+  int64_t in, out;
+  bool ok;
+};
+__device__ __forceinline__ PermIdx perm_pos(const PermAxis2& g, int64_t b, int u) {
+  PermIdx r;
+  if (g.comp) {
+    const int64_t a1 = u % g.n1, a2 = b * g.c2 + u / g.n1;
+    r.ok = (u < g.n1 * g.c2) && a2 < g.n2;
+    r.in = a1 * g.is1 + a2 * g.is2;
+    r.out = a1 * g.os1 + a2 * g.os2;
+  } else {
+    const int64_t a1 = b * TP + u;
+    r.ok = a1 < g.n1;
+    r.in = a1 * g.is1;
+    r.out = a1 * g.os1;
+  }
+  return r;
+}
+
+__global__ void __launch_bounds__(256) permute_tiled_kernel(const double* __restrict__ in,
+                                                            double* __restrict__ out, PermArgs a) {
+  __shared__ double tile[TP][TP + 1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8 threads
+  for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    int64_t rem = t;
+    const int64_t bx = rem % a.X.tiles; rem /= a.X.tiles;
+    const int64_t by = rem % a.Y.tiles; rem /= a.Y.tiles;
+    int64_t ib = 0, ob = 0;
+    for (int q = 0; q < a.nrest; ++q) {
+      const int64_t c = rem % a.rdim[q];
+      rem /= a.rdim[q];
+      ib += c * a.ris[q];
+      ob += c * a.ros[q];
+    }
+    const PermIdx px = perm_pos(a.X, bx, tx);   // x position of this lane (reads)
+    const PermIdx py = perm_pos(a.Y, by, tx);   // y position of this lane (writes)
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < TP; r += 8) {
+      const PermIdx yy = perm_pos(a.Y, by, ty + r);
+      if (px.ok && yy.ok) tile[ty + r][tx] = in[ib + px.in + yy.in];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < TP; r += 8) {
+      const PermIdx xx = perm_pos(a.X, bx, ty + r);
+      if (py.ok && xx.ok) out[ob + py.out + xx.out] = tile[tx][ty + r];
+    }
+  }
+}
+
+// fallback for permutations that keep a short input-fastest axis first
+struct PermArgsG {
+  int rank;
+  int64_t odims[6];
+  int64_t istride[6];
+  int64_t total;
+};
+__global__ void permute_generic_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                       PermArgsG a) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < a.total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     int64_t rem = idx, off = 0;
@@ -66,6 +141,25 @@ __global__ void permute_kernel(const double* __restrict__ in, double* __restrict
       }
     }
     out[idx] = in[off];
+  }
+}
+
+// contiguous runs (the output-fastest axis is the input-fastest axis)
+__global__ void __launch_bounds__(256) permute_runs_kernel(const double* __restrict__ in,
+                                                           double* __restrict__ out, PermArgs a) {
+  const int64_t run = a.X.n1, tiles_x = a.X.tiles;
+  for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    int64_t rem = t;
+    const int64_t bx = rem % tiles_x; rem /= tiles_x;
+    int64_t ib = 0, ob = 0;
+    for (int q = 0; q < a.nrest; ++q) {
+      const int64_t c = rem % a.rdim[q];
+      rem /= a.rdim[q];
+      ib += c * a.ris[q];
+      ob += c * a.ros[q];
+    }
+    const int64_t x = bx * 256 + threadIdx.x;
+    if (x < run) out[ob + x] = in[ib + x];
   }
 }
 
@@ -165,28 +259,117 @@ void fill_zero(cudaStream_t st, double* p, int64_t n) {
 void permute(cudaStream_t st, const double* in, double* out, int rank, const int64_t* dims,
              const int* perm) {
   if (rank < 1 || rank > 6) throw ValueError("permute rank must be 1..6");
-  int64_t istr[6];
-  int64_t s = 1;
-  for (int q = 0; q < rank; ++q) { istr[q] = s; s *= dims[q]; }
-  PermArgs a;
-  a.rank = rank;
-  a.total = s;
-  bool identity = true;
-  for (int q = 0; q < 6; ++q) { a.odims[q] = 1; a.istride[q] = 0; }
-  for (int q = 0; q < rank; ++q) {
-    a.odims[q] = dims[perm[q]];
-    a.istride[q] = istr[perm[q]];
-    if (perm[q] != q && dims[perm[q]] != 1) identity = false;
+  int64_t total = 1;
+  for (int q = 0; q < rank; ++q) total *= dims[q];
+  if (total == 0) return;
+  // canonical form: drop unit axes, merge input axes k, k+1 that are also
+  // consecutive in the output
+  int64_t n[6];
+  int p[6];        // output axis q <- canonical input axis p[q]
+  int nr = 0;
+  {
+    int map[6];
+    int64_t nd[6];
+    int kept = 0;
+    for (int k = 0; k < rank; ++k) {
+      map[k] = -1;
+      if (dims[k] != 1) { map[k] = kept; nd[kept++] = dims[k]; }
+    }
+    int op[6], no = 0;
+    for (int q = 0; q < rank; ++q)
+      if (map[perm[q]] >= 0) op[no++] = map[perm[q]];
+    // merge: output-consecutive pairs (k, k+1) of input axes
+    int grp[6];
+    for (int k = 0; k < kept; ++k) grp[k] = k;
+    for (int q = 0; q + 1 < no; ++q)
+      if (op[q + 1] == op[q] + 1) grp[op[q + 1]] = grp[op[q]];
+    int cid[6];
+    for (int k = 0; k < kept; ++k) {
+      if (grp[k] == k) { cid[k] = nr; n[nr++] = nd[k]; }
+      else { cid[k] = cid[grp[k]]; n[cid[k]] *= nd[k]; }
+    }
+    int np = 0;
+    for (int q = 0; q < no; ++q)
+      if (grp[op[q]] == op[q]) p[np++] = cid[op[q]];
   }
-  if (s == 0) return;
-  if (identity) {
-    // only unit axes move: the memory image is unchanged
-    CK(cudaMemcpyAsync(out, in, sizeof(double) * s, cudaMemcpyDeviceToDevice, st));
+  if (nr <= 1) {
+    CK(cudaMemcpyAsync(out, in, sizeof(double) * total, cudaMemcpyDeviceToDevice, st));
     return;
   }
-  permute_kernel<<<grid_for(s), 256, 0, st>>>(in, out, a);
-  CK_LAUNCH();
-  note_launch();
+  int64_t is[6], os[6];
+  {
+    int64_t s = 1;
+    for (int k = 0; k < nr; ++k) { is[k] = s; s *= n[k]; }
+    s = 1;
+    for (int q = 0; q < nr; ++q) { os[p[q]] = s; s *= n[p[q]]; }
+  }
+  auto launch_generic = [&]() {
+    PermArgsG g{};
+    g.rank = nr;
+    g.total = total;
+    for (int q = 0; q < 6; ++q) { g.odims[q] = 1; g.istride[q] = 0; }
+    for (int q = 0; q < nr; ++q) { g.odims[q] = n[p[q]]; g.istride[q] = is[p[q]]; }
+    permute_generic_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 148 * 16)),
+                             256, 0, st>>>(in, out, g);
+    CK_LAUNCH();
+    note_launch();
+  };
+  PermArgs a{};
+  bool used[6] = {false, false, false, false, false, false};
+  auto rest_and_launch = [&](bool runs) {
+    a.nrest = 0;
+    a.ntiles = a.X.tiles * (runs ? 1 : a.Y.tiles);
+    for (int k = 0; k < nr; ++k) {
+      if (used[k]) continue;
+      a.rdim[a.nrest] = n[k];
+      a.ris[a.nrest] = is[k];
+      a.ros[a.nrest] = os[k];
+      a.ntiles *= n[k];
+      ++a.nrest;
+    }
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(a.ntiles, 148 * 16));
+    if (runs) permute_runs_kernel<<<blocks, 256, 0, st>>>(in, out, a);
+    else permute_tiled_kernel<<<blocks, 256, 0, st>>>(in, out, a);
+    CK_LAUNCH();
+    note_launch();
+  };
+  if (p[0] == 0) {
+    // runs along the input-fastest axis
+    if (n[0] < 64) { launch_generic(); return; }
+    a.X.n1 = n[0];
+    a.X.tiles = cdiv(n[0], 256);
+    used[0] = true;
+    rest_and_launch(true);
+    return;
+  }
+  // X group: input axis 0 (+ axis 1 when axis 0 is short and axis 1 is not
+  // the output-fastest axis)
+  auto set_group = [&](PermAxis2& g, int k1, int k2, bool is_x) {
+    g.n1 = n[k1];
+    g.is1 = is[k1];
+    g.os1 = os[k1];
+    g.comp = k2 >= 0;
+    used[k1] = true;
+    if (g.comp) {
+      g.n2 = n[k2];
+      g.is2 = is[k2];
+      g.os2 = os[k2];
+      g.c2 = std::max<int64_t>(1, TP / g.n1);
+      g.tiles = cdiv(g.n2, g.c2);
+      used[k2] = true;
+    } else {
+      g.n2 = 1; g.c2 = 1; g.is2 = 0; g.os2 = 0;
+      g.tiles = cdiv(g.n1, TP);
+    }
+    (void)is_x;
+  };
+  const int y1 = p[0];
+  int x2 = -1, y2 = -1;
+  if (n[0] < TP && nr > 2 && y1 != 1) x2 = 1;
+  if (n[y1] < TP && nr > 2 && p[1] != 0 && p[1] != x2) y2 = p[1];
+  set_group(a.X, 0, x2, true);
+  set_group(a.Y, y1, y2, false);
+  rest_and_launch(false);
 }
 
 void frob_norm(cudaStream_t st, const double* x, int64_t n, double* out_dev) {

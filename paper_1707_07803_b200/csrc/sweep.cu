@@ -103,6 +103,28 @@ Core left_absorb(cudaStream_t st, const double* C, int64_t m, const PEntry& e) {
   return n;
 }
 
+double left_absorb_flops(const PEntry& e, int64_t m) {
+  if (e.expl) return 2.0 * m * e.R() * e.I() * e.K() * e.S();
+  const double Ra = e.a.R(), I = e.a.I(), Jc = e.a.J(), Sa = e.a.S();
+  const double Rb = e.b.R(), K = e.b.J(), Sb = e.b.S();
+  return 2.0 * m * Ra * Rb * Jc * K * Sb + 2.0 * m * Ra * Jc * I * Sa * K * Sb;
+}
+
+// contraction-order costs of right_absorb_t: B·L first or A·L first
+void right_absorb_orders(const PEntry& e, int64_t r, double& f_bl, double& f_al) {
+  const double Ra = e.a.R(), I = e.a.I(), Jc = e.a.J(), Sa = e.a.S();
+  const double Rb = e.b.R(), K = e.b.J(), Sb = e.b.S();
+  f_bl = 2.0 * (Rb * Jc * K * Sb * Sa * r + Ra * I * Jc * Sa * Rb * K * r);
+  f_al = 2.0 * (Ra * I * Jc * Sa * Sb * r + Ra * I * Jc * Sb * r * Rb * K);
+}
+
+double right_absorb_flops(const PEntry& e, int64_t r) {
+  if (e.expl) return 2.0 * e.R() * e.I() * e.K() * e.S() * r;
+  double f_bl, f_al;
+  right_absorb_orders(e, r, f_bl, f_al);
+  return std::min(f_bl, f_al);
+}
+
 // Mt (I·K·r x R) = (P x_4 Lt^T)^T with Lt (r x S, ld r), i.e. the transposed
 // unfolding of the core P·Lt^T that the pre-pass factors.
 void right_absorb_t(cudaStream_t st, const PEntry& e, const double* Lt, int64_t r, double* Mt) {
@@ -121,6 +143,42 @@ void right_absorb_t(cudaStream_t st, const PEntry& e, const double* Lt, int64_t 
   DBuf<double> tb, ta;
   const double* Bu = layout(st, e.b, false, tb);   // (b, jc, k, b')
   const double* Au = layout(st, e.a, false, ta);   // (a, i, jc, a')
+  // contraction order: B·L first (cost ~ Ra·I·Jc·Sa·Rb·K·r) or A·L first
+  // (~ Ra·I·Jc·Sa·Sb·r); the latter wins when op(A) carries the large ranks
+  // (B = Q^T A at config 5: Ra = Sa = 4096, Rb = Sb = 16)
+  double f_bl, f_al;
+  right_absorb_orders(e, r, f_bl, f_al);
+  if (f_al < f_bl) {
+    // V[a, i, jc, s, b'] = sum_a' A[a, i, jc, a'] Lt[s, a' + Sa·b']  (batched over b')
+    DBuf<double> V((size_t)(Ra * I * Jc * r * Sb), st);
+    dgemm(st, false, true, Ra * I * Jc, r, Sa, 1.0, Au, Ra * I * Jc, Lt, r, 0.0, V.get(),
+          Ra * I * Jc, Sb, 0, r * Sa, Ra * I * Jc * r);
+    // V'[a, i, s, jc, b']
+    DBuf<double> Vp((size_t)(Ra * I * Jc * r * Sb), st);
+    {
+      int64_t dims[5] = {Ra, I, Jc, r, Sb};
+      int perm[5] = {0, 1, 3, 2, 4};
+      permute(st, V.get(), Vp.get(), 5, dims, perm);
+    }
+    V.reset();
+    // Bv[jc, b', b, k] = B[b, jc, k, b']
+    DBuf<double> Bv((size_t)(Rb * Jc * K * Sb), st);
+    {
+      int64_t dims[4] = {Rb, Jc, K, Sb};
+      int perm[4] = {1, 3, 0, 2};
+      permute(st, Bu, Bv.get(), 4, dims, perm);
+    }
+    // M''[a, i, s, b, k] = sum_{jc, b'} V'[a, i, s, jc, b'] Bv[jc, b', b, k]
+    DBuf<double> Mpp((size_t)(Ra * I * r * Rb * K), st);
+    dgemm(st, false, false, Ra * I * r, Rb * K, Jc * Sb, 1.0, Vp.get(), Ra * I * r, Bv.get(),
+          Jc * Sb, 0.0, Mpp.get(), Ra * I * r);
+    Vp.reset();
+    // Mt[i, k, s, a, b]
+    int64_t dims[5] = {Ra, I, r, Rb, K};
+    int perm[5] = {1, 4, 2, 0, 3};
+    permute(st, Mpp.get(), Mt, 5, dims, perm);
+    return;
+  }
   // L'[b', a', s] = Lt[s, a' + Sa·b']
   DBuf<double> Lp((size_t)(Sb * Sa * r), st);
   {
@@ -263,7 +321,9 @@ Cores orthogonalize_product(cudaStream_t st, const Cores* a, bool ta, const Core
       // pick the smaller intermediate: P x_4 Lt^T (R·IK·rr) or C x_1 P (m·IK·S)
       const int64_t IK = P[k].I() * P[k].K();
       const int64_t R = P[k].R(), S = P[k].S();
-      const bool right_first = (k == 0) || (double)R * rr <= (double)m * S;
+      const bool right_first =
+          (k == 0) || right_absorb_flops(P[k], rr) + 2.0 * m * IK * rr * R <=
+                          left_absorb_flops(P[k], m) + 2.0 * m * IK * S * rr;
       if (right_first) {
         DBuf<double> Mt((size_t)(IK * rr * R), st);
         right_absorb_t(st, P[k], Lt.get(), rr, Mt.get());
