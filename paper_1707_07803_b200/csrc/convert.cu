@@ -27,7 +27,6 @@ constexpr int CT = 256;              // threads per tile CTA
 constexpr int ITEMS = 16;            // keys per thread
 constexpr int TILE = CT * ITEMS;     // 4096 keys per tile
 constexpr int WARPS = CT / 32;
-constexpr int WITEMS = 32 * ITEMS;   // keys per warp (512)
 constexpr int RADIX = 256;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -146,76 +145,112 @@ __global__ void split_keys(SplitArgs a) {
   }
 }
 
-// ---------------- radix sort passes ----------------------------------------
-// warp-private digit counters, walked in item order (stable, atomics-free)
-__global__ void radix_hist(const uint64_t* __restrict__ key, int64_t n, int shift,
-                           unsigned* hist, int64_t ntiles) {
-  __shared__ unsigned wh[WARPS][RADIX];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int d = threadIdx.x; d < WARPS * RADIX; d += CT) (&wh[0][0])[d] = 0;
+// ---------------- radix sort ------------------------------------------------
+// ---------------- onesweep LSD passes (decoupled look-back) ----------------
+// One read of the keys computes the digit histograms of every pass; each
+// pass is then ONE kernel: tiles take ids from an atomic counter (launch
+// order, so a tile only ever waits on tiles already running), rank their
+// keys exactly as radix_scatter does, publish per-digit tile counts and
+// find their global per-digit offsets by looking back over the preceding
+// tiles' published counts/prefixes.  The atomics only schedule and signal:
+// ranks and offsets are the same as the two-kernel pass, so the sort stays
+// stable and the output bit-deterministic.
+constexpr int MAXPASS = 8;
+// smaller tiles than the two-kernel passes: 8 keys per thread keep the
+// kernel at <= 64 registers, 4 CTAs (32 warps) per SM to hide the loads
+constexpr int OS_ITEMS = 8, OS_TILE = CT * OS_ITEMS, OS_WITEMS = 32 * OS_ITEMS;
+constexpr size_t OS_SMEM = (size_t)OS_TILE * (sizeof(uint64_t) + sizeof(unsigned));
+constexpr unsigned long long OS_AGG = 1ull << 62, OS_PRE = 2ull << 62,
+                             OS_VAL = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(CT) onesweep_hist(const uint64_t* __restrict__ key, int64_t n,
+                                                    int npass, int shift0,
+                                                    unsigned* __restrict__ part,
+                                                    uint64_t low_mask, int* unsorted) {
+  // histograms of passes p = 0.. at shift 8p and, when low_mask != 0, of
+  // the passes at shift0 + 8p (used when the keys are already
+  // non-decreasing in their low bits, checked here in the same read)
+  __shared__ unsigned h[2 * MAXPASS][RADIX];
+  __shared__ int s_uns;
+  for (int i = threadIdx.x; i < 2 * MAXPASS * RADIX; i += CT) (&h[0][0])[i] = 0;
+  if (threadIdx.x == 0) s_uns = 0;
   __syncthreads();
-  const int64_t wbase = blockIdx.x * (int64_t)TILE + warp * WITEMS;
-  // all loads in flight before the ranking loop (its __syncwarp()s are
-  // memory fences that would otherwise expose one load latency per item)
-  unsigned digs[ITEMS];
-#pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {
-    const int64_t i = wbase + it * 32 + lane;
-    digs[it] = i < n ? (unsigned)((key[i] >> shift) & (RADIX - 1)) : RADIX;  // RADIX = invalid
+  bool uns = false;
+  const int nsets = low_mask ? 2 : 1;
+  for (int64_t i = blockIdx.x * (int64_t)CT + threadIdx.x; i < n; i += (int64_t)gridDim.x * CT) {
+    const uint64_t k = key[i];
+    for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(k >> (8 * p)) & (RADIX - 1)], 1u);
+    if (low_mask) {
+      for (int p = 0; p < npass; ++p)
+        atomicAdd(&h[MAXPASS + p][(k >> (shift0 + 8 * p)) & (RADIX - 1)], 1u);
+      if (i > 0 && (key[i - 1] & low_mask) > (k & low_mask)) uns = true;
+    }
   }
-#pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {
-    const unsigned dig = digs[it];
-    const bool valid = dig < RADIX;
-    unsigned peers = __match_any_sync(0xffffffffu, dig);
-    int leader = __ffs(peers) - 1;
-    if (valid && lane == leader) wh[warp][dig] += __popc(peers);
-    __syncwarp();
-  }
+  if (uns) s_uns = 1;
   __syncthreads();
-  for (int d = threadIdx.x; d < RADIX; d += CT) {
-    unsigned s = 0;
-    for (int w = 0; w < WARPS; ++w) s += wh[w][d];
-    hist[(int64_t)d * ntiles + blockIdx.x] = s;   // digit-major for the scan
-  }
+  for (int q = 0; q < nsets; ++q)
+    for (int i = threadIdx.x; i < npass * RADIX; i += CT)
+      part[((int64_t)blockIdx.x * nsets + q) * npass * RADIX + i] = h[q * MAXPASS + i / RADIX][i % RADIX];
+  if (threadIdx.x == 0 && s_uns) atomicOr(unsorted, 1);
 }
 
-// Stable scatter of one 8-bit digit pass.  Keys are ranked inside the tile
-// (warp-private counters, then a digit-major prefix), staged in shared
-// memory in digit order, and written out as contiguous per-digit runs so
-// the global stores coalesce (a direct scatter would touch one 32-byte
-// sector per 8-byte key).
-constexpr size_t SCATTER_SMEM = (size_t)TILE * (sizeof(uint64_t) + sizeof(unsigned));
+// per pass: digit totals summed over the histogram CTAs in a fixed order,
+// then the exclusive scan over digits -> global digit offsets
+__global__ void onesweep_offsets(const unsigned* __restrict__ part, int nblk, int nsets, int set,
+                                 int npass, int64_t* __restrict__ doff) {
+  __shared__ int64_t tot[RADIX];
+  const int p = blockIdx.x, d = threadIdx.x;
+  int64_t s = 0;
+  for (int b = 0; b < nblk; ++b) s += part[(((int64_t)b * nsets + set) * npass + p) * RADIX + d];
+  tot[d] = s;
+  __syncthreads();
+  if (d == 0) {
+    int64_t acc = 0;
+    for (int q = 0; q < RADIX; ++q) { const int64_t v = tot[q]; tot[q] = acc; acc += v; }
+  }
+  __syncthreads();
+  doff[p * RADIX + d] = tot[d];
+}
 
-__global__ void __launch_bounds__(CT) radix_scatter(const uint64_t* __restrict__ key,
-                                                    const unsigned* __restrict__ pay, int64_t n,
-                                                    int shift, const int64_t* __restrict__ offs,
-                                                    int64_t ntiles, uint64_t* __restrict__ key_out,
-                                                    unsigned* __restrict__ pay_out) {
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+
+__global__ void __launch_bounds__(CT, 4) onesweep_scatter(
+    const uint64_t* __restrict__ key, const unsigned* __restrict__ pay, int64_t n, int shift,
+    const int64_t* __restrict__ doff, unsigned long long* status, unsigned* tile_ctr,
+    uint64_t* __restrict__ key_out, unsigned* __restrict__ pay_out) {
   extern __shared__ __align__(16) unsigned char ssm[];
   uint64_t* skey = reinterpret_cast<uint64_t*>(ssm);
-  unsigned* spay = reinterpret_cast<unsigned*>(ssm + (size_t)TILE * sizeof(uint64_t));
+  unsigned* spay = reinterpret_cast<unsigned*>(ssm + (size_t)OS_TILE * sizeof(uint64_t));
   __shared__ unsigned wh[WARPS][RADIX];
   __shared__ unsigned dstart[RADIX];
   __shared__ int64_t tbase[RADIX];
+  __shared__ unsigned s_tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   for (int d = threadIdx.x; d < WARPS * RADIX; d += CT) (&wh[0][0])[d] = 0;
-  for (int d = threadIdx.x; d < RADIX; d += CT) tbase[d] = offs[(int64_t)d * ntiles + blockIdx.x];
   __syncthreads();
-  const int64_t tstart = blockIdx.x * (int64_t)TILE;
-  const int tcount = (int)((n - tstart) < TILE ? (n - tstart) : TILE);
-  const int64_t wbase = tstart + warp * WITEMS;
-  uint64_t k[ITEMS];
-  unsigned pv[ITEMS], rank[ITEMS];
+  const int64_t tile = s_tile;
+  const int64_t tstart = tile * OS_TILE;
+  const int tcount = (int)((n - tstart) < OS_TILE ? (n - tstart) : OS_TILE);
+  const int64_t wbase = tstart + warp * OS_WITEMS;
+  uint64_t k[OS_ITEMS];
+  unsigned pv[OS_ITEMS], rank[OS_ITEMS];
 #pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {   // all loads first (see radix_hist)
+  for (int it = 0; it < OS_ITEMS; ++it) {
     const int64_t i = wbase + it * 32 + lane;
     const bool valid = i < n;
     k[it] = valid ? key[i] : 0;
     pv[it] = valid ? pay[i] : 0;
   }
 #pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {
+  for (int it = 0; it < OS_ITEMS; ++it) {
     const bool valid = wbase + it * 32 + lane < n;
     unsigned dig = valid ? (unsigned)((k[it] >> shift) & (RADIX - 1)) : RADIX;
     unsigned peers = __match_any_sync(0xffffffffu, dig);
@@ -227,15 +262,29 @@ __global__ void __launch_bounds__(CT) radix_scatter(const uint64_t* __restrict__
     __syncwarp();
   }
   __syncthreads();
-  // per digit: exclusive prefix over warps, and the digit's tile total
   if (threadIdx.x < RADIX) {
     const int d = threadIdx.x;
     unsigned acc = 0;
     for (int w = 0; w < WARPS; ++w) { unsigned v = wh[w][d]; wh[w][d] = acc; acc += v; }
     dstart[d] = acc;
+    // publish this tile's count, look back for the prefix, publish the prefix
+    unsigned long long* st = status + tile * RADIX + d;
+    int64_t prefix = 0;
+    if (tile == 0) {
+      st_volatile_u64(st, OS_PRE | (unsigned long long)acc);
+    } else {
+      st_volatile_u64(st, OS_AGG | (unsigned long long)acc);
+      int64_t j = tile - 1;
+      while (true) {
+        const unsigned long long v = ld_volatile_u64(status + j * RADIX + d);
+        if (v & OS_PRE) { prefix += (int64_t)(v & OS_VAL); break; }
+        if (v & OS_AGG) { prefix += (int64_t)(v & OS_VAL); --j; }
+      }
+      st_volatile_u64(st, OS_PRE | (unsigned long long)(prefix + acc));
+    }
+    tbase[d] = doff[d] + prefix;
   }
   __syncthreads();
-  // exclusive scan of the 256 digit totals (Hillis-Steele, one value/thread)
   {
     unsigned v = threadIdx.x < RADIX ? dstart[threadIdx.x] : 0;
     const unsigned orig = v;
@@ -249,7 +298,7 @@ __global__ void __launch_bounds__(CT) radix_scatter(const uint64_t* __restrict__
   }
   __syncthreads();
 #pragma unroll
-  for (int it = 0; it < ITEMS; ++it) {
+  for (int it = 0; it < OS_ITEMS; ++it) {
     int64_t i = wbase + it * 32 + lane;
     if (i < n) {
       unsigned dig = (unsigned)((k[it] >> shift) & (RADIX - 1));
@@ -289,30 +338,53 @@ __global__ void head_counts(const uint64_t* __restrict__ key, int64_t n, unsigne
   }
 }
 
-__global__ void assign_ids(const uint64_t* __restrict__ key, const unsigned* __restrict__ pos,
-                           int64_t n, const int64_t* __restrict__ tile_off, int64_t* uniq,
-                           int64_t* ti, int64_t pos_base) {
-  __shared__ unsigned wsum[WARPS];
+__global__ void __launch_bounds__(CT) assign_ids(const uint64_t* __restrict__ key,
+                                                 const unsigned* __restrict__ pos, int64_t n,
+                                                 const int64_t* __restrict__ tile_off,
+                                                 int64_t* uniq, int64_t* ti, int64_t pos_base) {
+  // items i = base + it*CT + t; every load is issued before any rank is
+  // formed, and one barrier publishes the per-(item row, warp) head counts
+  __shared__ unsigned wcnt[ITEMS][WARPS];
   const int64_t base = blockIdx.x * (int64_t)TILE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t run = tile_off[blockIdx.x];  // heads strictly before this tile
+  uint64_t k[ITEMS], kp[ITEMS];
+  unsigned pv[ITEMS];
+#pragma unroll
   for (int it = 0; it < ITEMS; ++it) {
-    int64_t i = base + it * CT + threadIdx.x;
-    bool valid = i < n;
-    bool head = valid && (i == 0 || key[i] != key[i - 1]);
-    unsigned ball = __ballot_sync(0xffffffffu, head);
-    if (lane == 0) wsum[warp] = __popc(ball);
-    __syncthreads();
+    const int64_t i = base + it * CT + threadIdx.x;
+    const bool valid = i < n;
+    k[it] = valid ? key[i] : 0;
+    kp[it] = (valid && i > 0) ? key[i - 1] : ~k[it];
+    pv[it] = valid ? pos[i] : 0;
+  }
+  unsigned ball[ITEMS];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const int64_t i = base + it * CT + threadIdx.x;
+    const bool head = i < n && k[it] != kp[it];
+    ball[it] = __ballot_sync(0xffffffffu, head);
+    if (lane == 0) wcnt[it][warp] = __popc(ball[it]);
+  }
+  __syncthreads();
+  int64_t run = tile_off[blockIdx.x];  // heads strictly before this tile
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
     unsigned before = 0, total = 0;
-    for (int w = 0; w < WARPS; ++w) { if (w < warp) before += wsum[w]; total += wsum[w]; }
-    if (valid) {
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      const unsigned c = wcnt[it][w];
+      before += (w < warp) ? c : 0;
+      total += c;
+    }
+    const int64_t i = base + it * CT + threadIdx.x;
+    if (i < n) {
+      const bool head = (ball[it] >> lane) & 1u;
       // id = (#heads at or before i) - 1
-      int64_t id = run + before + __popc(ball & lanemask_lt()) + (head ? 1 : 0) - 1;
-      if (head) uniq[id] = (int64_t)key[i];
-      ti[(int64_t)pos[i] - pos_base] = id;
+      const int64_t id = run + before + __popc(ball[it] & lanemask_lt()) + (head ? 1 : 0) - 1;
+      if (head) uniq[id] = (int64_t)k[it];
+      ti[(int64_t)pv[it] - pos_base] = id;
     }
     run += total;
-    __syncthreads();
   }
 }
 
@@ -353,28 +425,58 @@ int key_bits(uint64_t max_key) {
 }
 
 void radix_sort_pairs(cudaStream_t st, uint64_t* key, unsigned* pay, int64_t n, int bits,
-                      uint64_t* key_tmp, unsigned* pay_tmp, bool& result_in_tmp) {
+                      uint64_t* key_tmp, unsigned* pay_tmp, bool& result_in_tmp, int low_bits) {
   result_in_tmp = false;
   if (n <= 1 || bits == 0) return;
-  const int64_t ntiles = cdiv(n, TILE);
+  const int64_t ntiles = cdiv(n, OS_TILE);
+  int npass = (bits + 7) / 8;
+  if (npass > MAXPASS) throw ValueError("sort key wider than 64 bits");
   static const bool attr = [] {   // thread-safe one-time setup
-    CK(cudaFuncSetAttribute(radix_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)SCATTER_SMEM));
+    CK(cudaFuncSetAttribute(onesweep_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)OS_SMEM));
     return true;
   }();
   (void)attr;
-  DBuf<unsigned> hist((size_t)RADIX * ntiles, st);
-  DBuf<int64_t> offs((size_t)RADIX * ntiles, st), total(1, st);
+  // presorted low bits: when the keys are already non-decreasing in their
+  // low `low_bits` bits (row-sorted COO input: key = br + nrb*bc with nrb =
+  // 2^low_bits, br non-decreasing), a stable sort on the high bits alone
+  // yields the full key order
+  const bool try_low = low_bits > 0 && low_bits < bits && (bits - low_bits + 7) / 8 < npass;
+  const uint64_t low_mask = try_low ? ((1ull << low_bits) - 1) : 0;
+  const int nsets = try_low ? 2 : 1;
+  const int hblk = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, CT * 16), 148 * 4));
+  DBuf<unsigned> part((size_t)hblk * nsets * npass * RADIX, st), ctr(npass, st);
+  DBuf<int64_t> doff((size_t)npass * RADIX, st);
+  DBuf<int> uns(1, st);
+  CK(cudaMemsetAsync(ctr.get(), 0, sizeof(unsigned) * npass, st));
+  CK(cudaMemsetAsync(uns.get(), 0, sizeof(int), st));
+  onesweep_hist<<<hblk, CT, 0, st>>>(key, n, npass, low_bits, part.get(), low_mask, uns.get());
+  CK_LAUNCH();
+  int set = 0, shift0 = 0;
+  if (try_low) {
+    int h_uns = 1;
+    CK(cudaMemcpyAsync(&h_uns, uns.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!h_uns) {
+      set = 1;
+      shift0 = low_bits;
+      npass = (bits - low_bits + 7) / 8;
+    }
+  }
+  onesweep_offsets<<<npass, RADIX, 0, st>>>(part.get(), hblk, nsets, set,
+                                            (bits + 7) / 8, doff.get());
+  CK_LAUNCH();
+  note_launch(2);
+  DBuf<unsigned long long> status((size_t)ntiles * RADIX, st);
   uint64_t *ks = key, *kd = key_tmp;
   unsigned *ps = pay, *pd = pay_tmp;
-  for (int shift = 0; shift < bits; shift += 8) {
-    radix_hist<<<(int)ntiles, CT, 0, st>>>(ks, n, shift, hist.get(), ntiles);
+  for (int p = 0; p < npass; ++p) {
+    CK(cudaMemsetAsync(status.get(), 0, sizeof(unsigned long long) * ntiles * RADIX, st));
+    onesweep_scatter<<<(int)ntiles, CT, OS_SMEM, st>>>(ks, ps, n, shift0 + 8 * p,
+                                                       doff.get() + p * RADIX, status.get(),
+                                                       ctr.get() + p, kd, pd);
     CK_LAUNCH();
-    exclusive_scan_u32(st, hist.get(), RADIX * ntiles, offs.get(), total.get());
-    radix_scatter<<<(int)ntiles, CT, SCATTER_SMEM, st>>>(ks, ps, n, shift, offs.get(), ntiles, kd,
-                                                          pd);
-    CK_LAUNCH();
-    note_launch(2);
+    note_launch();
     std::swap(ks, kd);
     std::swap(ps, pd);
     result_in_tmp = !result_in_tmp;
@@ -412,7 +514,10 @@ ConvLocal convert_local(cudaStream_t st, const int64_t* row1, const int64_t* col
   note_launch();
   const uint64_t max_key = (uint64_t)(nrb * ncb - 1);
   bool in_tmp = false;
-  radix_sort_pairs(st, key.get(), pos.get(), nk, key_bits(max_key), key2.get(), pos2.get(), in_tmp);
+  // nrb a power of two: row-sorted input needs only the block-column bits
+  const int low = (nrb & (nrb - 1)) == 0 ? key_bits((uint64_t)(nrb - 1)) : 0;
+  radix_sort_pairs(st, key.get(), pos.get(), nk, key_bits(max_key), key2.get(), pos2.get(), in_tmp,
+                   low);
   const uint64_t* sk = in_tmp ? key2.get() : key.get();
   const unsigned* sp = in_tmp ? pos2.get() : pos.get();
   const int64_t t2 = grid_tiles(nk);

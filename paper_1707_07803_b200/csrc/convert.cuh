@@ -26,8 +26,12 @@ void level_digits(cudaStream_t st, const int64_t* uniq, int64_t rank, int64_t nr
 void exclusive_scan_u32(cudaStream_t st, const unsigned* in, int64_t n, int64_t* out,
                         int64_t* total_dev);
 int key_bits(uint64_t max_key);
+// stable LSD sort of (key, pay) on the low `bits` key bits; low_bits > 0
+// lets it skip the passes below bit low_bits when the keys are found
+// non-decreasing in those bits
 void radix_sort_pairs(cudaStream_t st, uint64_t* key, unsigned* pay, int64_t n, int bits,
-                      uint64_t* key_tmp, unsigned* pay_tmp, bool& result_in_tmp);
+                      uint64_t* key_tmp, unsigned* pay_tmp, bool& result_in_tmp,
+                      int low_bits = 0);
 
 }  // namespace mpob
 

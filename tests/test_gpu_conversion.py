@@ -84,6 +84,32 @@ def test_conversion_properties_large_random():
     assert res.rank == np.unique(key).size
 
 
+@pytest.mark.parametrize("order", ["shuffled", "row_sorted", "col_sorted"])
+def test_conversion_input_order(order):
+    """The sort skips the block-row digit passes when the kept keys already
+    arrive sorted by block row (row-sorted COO); any other order takes the
+    full-key sort.  Both must match the oracle bit for bit."""
+    m = _api()
+    from paper_1707_07803_b200.workloads import powerlaw_coo, square_plan
+    r, c, v = powerlaw_coo(1 << 17, seed=21)
+    rng = np.random.default_rng(5)
+    if order == "shuffled":
+        p = rng.permutation(r.size)
+    elif order == "col_sorted":
+        p = np.lexsort((r, c))
+    else:
+        p = np.arange(r.size)
+    r, c, v = r[p], c[p], v[p]
+    v[rng.integers(0, v.size, 1000)] = 0.0   # explicit zeros are dropped
+    plan = square_plan(17)
+    res = m.convert_structure(r, c, v, plan)
+    i1, j1, ti, vals, uniq = res.arrays()
+    st = orc.conversion_structure(r, c, v, plan.row_factors, plan.col_factors)
+    assert np.array_equal(st.uniq, uniq) and np.array_equal(st.ti, ti)
+    assert np.array_equal(st.i1, i1) and np.array_equal(st.j1, j1)
+    assert np.array_equal(st.values, vals)
+
+
 def test_conversion_empty_and_zero_values():
     m = _api()
     a = m.SparseMatrixCoo(8, 8, [], [], [])
