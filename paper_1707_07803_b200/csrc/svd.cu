@@ -210,6 +210,12 @@ __device__ __forceinline__ void mmP(const double* S, const double* B, double (&a
   }
 }
 
+#ifdef MPO_EIG_PROF
+__device__ unsigned g_eig_launch = 0;
+#define EIG_T(i) if (t == 0) tclk[i] = clock64();
+#else
+#define EIG_T(i)
+#endif
 template <int JB>
 __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
   using K = JK<JB>;
@@ -225,10 +231,16 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
   __shared__ unsigned char s_blk[NBLK][2];
   // rotations double-buffered by round parity: J's update for round r-1
   // runs (warps 1..) while warp 0 computes round r's rotations
-  __shared__ double rc[2][NPR], rs[2][NPR], rdp[NPR], rdq[NPR];
+  // every inner round's rotations are kept (J is accumulated from them once
+  // per inner sweep, row-parallel, off the round-to-round critical path)
+  __shared__ double rc[P2 - 1][NPR], rs[P2 - 1][NPR], rdp[NPR], rdq[NPR];
   __shared__ int rflag[2][NPR];
   __shared__ int s_skip;
   const int t = threadIdx.x, pair = blockIdx.x, lane = t & 31, warp = t >> 5;
+#ifdef MPO_EIG_PROF
+  long long tclk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+  EIG_T(0)
   {
     // sum the row-split partial Grams in split order (loads issued first)
     constexpr int PER = P2 * P2 / ET;
@@ -252,6 +264,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     }
   }
   if (t == 0) s_skip = 1;
+  EIG_T(1)
   __syncthreads();   // only the upper triangle of G is read from here on
   const double gfl = a.floorc * (*a.fro) * (*a.fro);   // (c eps ||X||_F)^2
   {
@@ -275,6 +288,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     if (a.skiplog) a.skiplog[(int64_t)a.round * gridDim.x + pair] = s_skip;
   }
   if (s_skip) return;
+  EIG_T(2)
   if (t == 0) *a.flag = 1;
 
   // cyclic two-sided Jacobi on G (parallel circle ordering), two phases per
@@ -310,27 +324,57 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     }
   }
   __syncthreads();
-  // J's columns p, q rotated by round rr's rotations (warps jw0.., strided)
-  auto j_update = [&](int rr, int jt, int jn) {
-    const int par = rr & 1;
-    for (int idx = jt; idx < P2 * NPR; idx += jn) {
-      const int w = idx / P2, row = idx % P2;
-      if (!rflag[par][w]) continue;
+  // J <- J R_0 R_1 ... R_{nr-1}: rows of J are independent, and the NPR
+  // rotations of one round act on disjoint column pairs, so each warp owns
+  // P2/NW rows and its lanes apply one rotation each per round, with only
+  // __syncwarp() between rounds
+  auto j_accumulate = [&](int nr) {
+    constexpr int NW = ET / 32, RW = P2 / NW, LPR = 32 / NPR, RPL = RW / LPR;
+    const int w = lane % NPR, row0 = warp * RW + lane / NPR;
+    for (int rr = 0; rr < nr; ++rr) {
       const int p = s_pq[rr][w][0], q = s_pq[rr][w][1];
-      const double c = rc[par][w], s = rs[par][w];
-      const double jp = J[row * GLD + p], jq = J[row * GLD + q];
-      J[row * GLD + p] = c * jp - s * jq;
-      J[row * GLD + q] = s * jp + c * jq;
+      const double c = rc[rr][w], sn = rs[rr][w];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int row = row0 + i * LPR;
+        const double jp = J[row * GLD + p], jq = J[row * GLD + q];
+        J[row * GLD + p] = c * jp - sn * jq;
+        J[row * GLD + q] = sn * jp + c * jq;
+      }
+      __syncwarp();
     }
   };
+  // per-thread static list of the 2x2 blocks this thread updates
+  constexpr int BPT = (NBLK + ET - 1) / ET;
+  int bu[BPT], bv[BPT];
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) {
+    const int idx = t + b * ET;
+    bu[b] = idx < NBLK ? s_blk[idx][0] : -1;
+    bv[b] = idx < NBLK ? s_blk[idx][1] : -1;
+  }
+  // cross-block schedule (rounds r: p = w, q = NPR + (w + r) mod NPR): J is
+  // held in registers -- lane w of a warp owns J[row][p_w] and J[row][q_w]
+  // for RPL rows, applies rotation w, and the q side moves one lane per
+  // round (q_w of round r+1 is q_{w+1} of round r): no shared-memory traffic
+  constexpr int NWJ = ET / 32, RW = P2 / NWJ, LPR = 32 / NPR, RPL = RW / LPR;
+  const int jw = lane % NPR, jrow0 = warp * RW + lane / NPR;
+  const int jsrc = (lane / NPR) * NPR + (jw + 1) % NPR;
+  double jp[RPL], jq[RPL];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int row = jrow0 + i * LPR;
+    jp[i] = row == jw ? 1.0 : 0.0;
+    jq[i] = row == NPR + jw ? 1.0 : 0.0;
+  }
+  EIG_T(3)
   for (int sweep = 0; sweep < a.inner; ++sweep) {
     int any = 0;
     for (int r = 0; r < nrounds; ++r) {
       const int par = r & 1;
-      if (warp > 0) {
-        if (r > 0) j_update(r - 1, t - 32, ET - 32);
-      } else if (t < NPR) {
-        const int p = s_pq[r][t][0], q = s_pq[r][t][1];
+      if (t < NPR) {
+        const int p = a.cross ? t : s_pq[r][t][0];
+        const int q = a.cross ? NPR + (t + r) % NPR : s_pq[r][t][1];
         const double gpp = G[p * GLD + p], gqq = G[q * GLD + q], gpq = G[p * GLD + q];
         const double pq = gpp * gqq;
         const bool rot = gpp > 0.0 && gqq > 0.0 && gpq * gpq > gfl * fmax(gpp, gqq) &&
@@ -360,25 +404,29 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
           c *= f;
           s *= f;
         }
-        rc[par][t] = c; rs[par][t] = s; rflag[par][t] = rot;
+        rc[r][t] = c; rs[r][t] = s; rflag[par][t] = rot;
         rdp[t] = fma(c * c, gpp, fma(-2.0 * c * s, gpq, s * s * gqq));
         rdq[t] = fma(s * s, gpp, fma(2.0 * c * s, gpq, c * c * gqq));
         any |= rot;
       }
       __syncthreads();
-      const int* rf = rflag[par];
-      const double *rcp = rc[par], *rsp = rs[par];
-      for (int idx = t; idx < NBLK; idx += ET) {
-        const int u = s_blk[idx][0], v = s_blk[idx][1];
-        if (!(rf[u] | rf[v])) continue;
-        const int pu = s_pq[r][u][0], qu = s_pq[r][u][1];
+      const double *rcp = rc[r], *rsp = rs[r];
+#pragma unroll
+      for (int b = 0; b < BPT; ++b) {
+        const int u = bu[b], v = bv[b];
+        if (u < 0) continue;
+        const int pu = a.cross ? u : s_pq[r][u][0];
+        const int qu = a.cross ? NPR + (u + r) % NPR : s_pq[r][u][1];
         if (u == v) {
+          if (!rflag[par][u]) continue;   // a non-rotating pair keeps its g_pq
           G[pu * GLD + pu] = rdp[u];
           G[qu * GLD + qu] = rdq[u];
-          G[pu * GLD + qu] = 0.0;   // pu < qu
+          G[min(pu, qu) * GLD + max(pu, qu)] = 0.0;
           continue;
         }
-        const int pv = s_pq[r][v][0], qv = s_pq[r][v][1];
+        // (c, s) = (1, 0) for a non-rotating pair: the update is then exact
+        const int pv = a.cross ? v : s_pq[r][v][0];
+        const int qv = a.cross ? NPR + (v + r) % NPR : s_pq[r][v][1];
         const double cu = rcp[u], su = rsp[u], cv = rcp[v], sv = rsp[v];
         // entry (a, b) of the symmetric G lives at min(a,b)*GLD + max(a,b)
         const int a00 = min(pu, pv) * GLD + max(pu, pv), a01 = min(pu, qv) * GLD + max(pu, qv);
@@ -391,9 +439,30 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
         G[a10] = su * x00 + cu * x10;
         G[a11] = su * x01 + cu * x11;
       }
+      if (a.cross) {
+        const double c = rcp[jw], sn = rsp[jw];
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const double x = jp[i], y = jq[i];
+          jp[i] = c * x - sn * y;
+          jq[i] = __shfl_sync(0xffffffffu, sn * x + c * y, jsrc);
+        }
+      }
       __syncthreads();
     }
-    j_update(nrounds - 1, t, ET);   // the last round's J update
+    EIG_T(4)
+    if (a.cross) {
+      // after NPR rounds the q side is back at q_w = NPR + w
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int row = jrow0 + i * LPR;
+        J[row * GLD + jw] = jp[i];
+        J[row * GLD + NPR + jw] = jq[i];
+      }
+    } else {
+      j_accumulate(nrounds);
+    }
+    EIG_T(5)
     if (!__syncthreads_or(any)) break;
   }
   // re-orthogonalise J: two Newton-Schulz steps J <- J - J (J^T J - I) / 2
@@ -432,8 +501,20 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     }
   }
   __syncthreads();
+  EIG_T(6)
   double* Jout = a.J + (int64_t)pair * P2 * P2;
   for (int idx = t; idx < P2 * P2; idx += ET) Jout[idx] = J[(idx / P2) * GLD + idx % P2];
+#ifdef MPO_EIG_PROF
+  EIG_T(7)
+  if (t == 0 && pair == 0) {
+    const unsigned L = atomicAdd(&g_eig_launch, 1u);
+    if (L % 97 == 5 && L < 2000)
+      printf("eigprof P2=%d cross=%d rounds=%d: sum %lld test %lld tables %lld inner %lld (%.0f/rd) jacc %lld ns %lld out %lld\n",
+             P2, a.cross, nrounds, tclk[1] - tclk[0], tclk[2] - tclk[1], tclk[3] - tclk[2],
+             tclk[4] - tclk[3], (double)(tclk[4] - tclk[3]) / nrounds, tclk[5] - tclk[4],
+             tclk[6] - tclk[5], tclk[7] - tclk[6]);
+  }
+#endif
 }
 
 // M[:, pair columns] <- M[:, pair columns] J for this CTA's rows, in place.
