@@ -482,6 +482,10 @@ def bench_conversion(args, torch, dist, rank, world, dev, barrier, max_over_rank
     peak_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6521.1
     achieved = compulsory / secs / 1e9 / world   # per GPU
+    try:
+        ctraffic = json.load(open(os.path.join(ROOT, "profiles", "r01_conv_traffic.json")))
+    except (OSError, ValueError):
+        ctraffic = {}
     # end to end: host COO in, host (i1, j1, ti, values, uniq) out
     import paper_1707_07803_b200 as m
     rs, cs_, vs = r[lo:hi], c[lo:hi], v[lo:hi]
@@ -502,8 +506,10 @@ def bench_conversion(args, torch, dist, rank, world, dev, barrier, max_over_rank
         "nnz": int(n), "blocks": int(blocks), "ms_per_step": secs * 1e3,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                      "frac": achieved / peak_hbm,
-                     "traffic": None, "algorithmic_bytes_per_step": compulsory,
-                     "note": "whole conversion (compaction + 6 radix passes + segment) timed; "
+                     "traffic": ctraffic.get("dram_bytes_per_step"),
+                     "traffic_source": ctraffic.get("source"),
+                     "algorithmic_bytes_per_step": compulsory,
+                     "note": "whole conversion (compaction + onesweep radix passes + segment) timed; "
                              "compulsory bytes 32 B/nnz + 8 B/block"},
         "e2e": {"value": (hi - lo) * world / e2e if world > 1 else n / e2e, "unit": "nnz/s",
                 "h2d_bytes_per_step": int(24 * (hi - lo)),

@@ -81,23 +81,36 @@ __global__ void scan_down(const unsigned* in, int64_t n, int64_t per, const int6
 }
 
 // ---------------- compaction + split + key ---------------------------------
-__global__ void count_nonzero_tiles(const double* __restrict__ val, int64_t n, unsigned* cnt) {
+__global__ void count_nonzero_tiles(const double* __restrict__ val,
+                                    const int64_t* __restrict__ row1, int64_t n, unsigned* cnt,
+                                    int* unsorted) {
+  // kept-entry counts per tile, and whether the rows arrive non-decreasing
+  // (then so do the block rows of the kept entries: the sort can skip them)
   __shared__ unsigned sh[WARPS];
+  __shared__ int s_uns;
+  if (threadIdx.x == 0) s_uns = 0;
   const int64_t base = blockIdx.x * (int64_t)TILE;
   unsigned c = 0;
+  bool uns = false;
 #pragma unroll
   for (int it = 0; it < ITEMS; ++it) {
     int64_t i = base + it * CT + threadIdx.x;
-    if (i < n && val[i] != 0.0) ++c;
+    if (i < n) {
+      if (val[i] != 0.0) ++c;
+      if (i > 0 && row1[i - 1] > row1[i]) uns = true;
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = c;
   __syncthreads();
+  if (uns) s_uns = 1;
+  __syncthreads();
   if (threadIdx.x == 0) {
     unsigned t = 0;
     for (int w = 0; w < WARPS; ++w) t += sh[w];
     cnt[blockIdx.x] = t;
+    if (s_uns) atomicOr(unsorted, 1);
   }
 }
 
@@ -165,51 +178,50 @@ constexpr unsigned long long OS_AGG = 1ull << 62, OS_PRE = 2ull << 62,
 
 __global__ void __launch_bounds__(CT) onesweep_hist(const uint64_t* __restrict__ key, int64_t n,
                                                     int npass, int shift0,
-                                                    unsigned* __restrict__ part,
-                                                    uint64_t low_mask, int* unsorted) {
-  // histograms of passes p = 0.. at shift 8p and, when low_mask != 0, of
-  // the passes at shift0 + 8p (used when the keys are already
-  // non-decreasing in their low bits, checked here in the same read)
-  __shared__ unsigned h[2 * MAXPASS][RADIX];
-  __shared__ int s_uns;
-  for (int i = threadIdx.x; i < 2 * MAXPASS * RADIX; i += CT) (&h[0][0])[i] = 0;
-  if (threadIdx.x == 0) s_uns = 0;
+                                                    unsigned* __restrict__ part) {
+  // histograms of the passes at shift0 + 8p, one read of the keys
+  __shared__ unsigned h[MAXPASS][RADIX];
+  for (int i = threadIdx.x; i < MAXPASS * RADIX; i += CT) (&h[0][0])[i] = 0;
   __syncthreads();
-  bool uns = false;
-  const int nsets = low_mask ? 2 : 1;
-  for (int64_t i = blockIdx.x * (int64_t)CT + threadIdx.x; i < n; i += (int64_t)gridDim.x * CT) {
-    const uint64_t k = key[i];
-    for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(k >> (8 * p)) & (RADIX - 1)], 1u);
-    if (low_mask) {
-      for (int p = 0; p < npass; ++p)
-        atomicAdd(&h[MAXPASS + p][(k >> (shift0 + 8 * p)) & (RADIX - 1)], 1u);
-      if (i > 0 && (key[i - 1] & low_mask) > (k & low_mask)) uns = true;
+  // 8 keys per thread in flight per step (a one-load loop is latency-bound)
+  constexpr int U = 8;
+  const int64_t stride = (int64_t)gridDim.x * CT;
+  for (int64_t i0 = blockIdx.x * (int64_t)CT + threadIdx.x; i0 < n; i0 += U * stride) {
+    uint64_t k[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      k[u] = i < n ? key[i] >> shift0 : ~0ull;
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k[u] != ~0ull)
+        for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(k[u] >> (8 * p)) & (RADIX - 1)], 1u);
   }
-  if (uns) s_uns = 1;
   __syncthreads();
-  for (int q = 0; q < nsets; ++q)
-    for (int i = threadIdx.x; i < npass * RADIX; i += CT)
-      part[((int64_t)blockIdx.x * nsets + q) * npass * RADIX + i] = h[q * MAXPASS + i / RADIX][i % RADIX];
-  if (threadIdx.x == 0 && s_uns) atomicOr(unsorted, 1);
+  for (int i = threadIdx.x; i < npass * RADIX; i += CT)
+    part[(int64_t)blockIdx.x * npass * RADIX + i] = (&h[0][0])[i];
 }
 
 // per pass: digit totals summed over the histogram CTAs in a fixed order,
 // then the exclusive scan over digits -> global digit offsets
-__global__ void onesweep_offsets(const unsigned* __restrict__ part, int nblk, int nsets, int set,
-                                 int npass, int64_t* __restrict__ doff) {
+__global__ void onesweep_offsets(const unsigned* __restrict__ part, int nblk, int npass,
+                                 int64_t* __restrict__ doff) {
   __shared__ int64_t tot[RADIX];
   const int p = blockIdx.x, d = threadIdx.x;
   int64_t s = 0;
-  for (int b = 0; b < nblk; ++b) s += part[(((int64_t)b * nsets + set) * npass + p) * RADIX + d];
+#pragma unroll 8
+  for (int b = 0; b < nblk; ++b) s += part[((int64_t)b * npass + p) * RADIX + d];
   tot[d] = s;
   __syncthreads();
-  if (d == 0) {
-    int64_t acc = 0;
-    for (int q = 0; q < RADIX; ++q) { const int64_t v = tot[q]; tot[q] = acc; acc += v; }
+  // exclusive scan over the 256 digits (Hillis-Steele)
+  for (int o = 1; o < RADIX; o <<= 1) {
+    const int64_t add = d >= o ? tot[d - o] : 0;
+    __syncthreads();
+    tot[d] += add;
+    __syncthreads();
   }
-  __syncthreads();
-  doff[p * RADIX + d] = tot[d];
+  doff[p * RADIX + d] = tot[d] - s;
 }
 
 __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
@@ -428,43 +440,26 @@ void radix_sort_pairs(cudaStream_t st, uint64_t* key, unsigned* pay, int64_t n, 
                       uint64_t* key_tmp, unsigned* pay_tmp, bool& result_in_tmp, int low_bits) {
   result_in_tmp = false;
   if (n <= 1 || bits == 0) return;
-  const int64_t ntiles = cdiv(n, OS_TILE);
-  int npass = (bits + 7) / 8;
+  // presorted low bits (the caller knows the keys are non-decreasing in
+  // their low `low_bits` bits): a stable sort on the high bits alone yields
+  // the full key order
+  const int shift0 = (low_bits > 0 && low_bits < bits) ? low_bits : 0;
+  const int npass = (bits - shift0 + 7) / 8;
   if (npass > MAXPASS) throw ValueError("sort key wider than 64 bits");
+  const int64_t ntiles = cdiv(n, OS_TILE);
   static const bool attr = [] {   // thread-safe one-time setup
     CK(cudaFuncSetAttribute(onesweep_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)OS_SMEM));
     return true;
   }();
   (void)attr;
-  // presorted low bits: when the keys are already non-decreasing in their
-  // low `low_bits` bits (row-sorted COO input: key = br + nrb*bc with nrb =
-  // 2^low_bits, br non-decreasing), a stable sort on the high bits alone
-  // yields the full key order
-  const bool try_low = low_bits > 0 && low_bits < bits && (bits - low_bits + 7) / 8 < npass;
-  const uint64_t low_mask = try_low ? ((1ull << low_bits) - 1) : 0;
-  const int nsets = try_low ? 2 : 1;
   const int hblk = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, CT * 16), 148 * 4));
-  DBuf<unsigned> part((size_t)hblk * nsets * npass * RADIX, st), ctr(npass, st);
+  DBuf<unsigned> part((size_t)hblk * npass * RADIX, st), ctr(npass, st);
   DBuf<int64_t> doff((size_t)npass * RADIX, st);
-  DBuf<int> uns(1, st);
   CK(cudaMemsetAsync(ctr.get(), 0, sizeof(unsigned) * npass, st));
-  CK(cudaMemsetAsync(uns.get(), 0, sizeof(int), st));
-  onesweep_hist<<<hblk, CT, 0, st>>>(key, n, npass, low_bits, part.get(), low_mask, uns.get());
+  onesweep_hist<<<hblk, CT, 0, st>>>(key, n, npass, shift0, part.get());
   CK_LAUNCH();
-  int set = 0, shift0 = 0;
-  if (try_low) {
-    int h_uns = 1;
-    CK(cudaMemcpyAsync(&h_uns, uns.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (!h_uns) {
-      set = 1;
-      shift0 = low_bits;
-      npass = (bits - low_bits + 7) / 8;
-    }
-  }
-  onesweep_offsets<<<npass, RADIX, 0, st>>>(part.get(), hblk, nsets, set,
-                                            (bits + 7) / 8, doff.get());
+  onesweep_offsets<<<npass, RADIX, 0, st>>>(part.get(), hblk, npass, doff.get());
   CK_LAUNCH();
   note_launch(2);
   DBuf<unsigned long long> status((size_t)ntiles * RADIX, st);
@@ -491,12 +486,16 @@ ConvLocal convert_local(cudaStream_t st, const int64_t* row1, const int64_t* col
   const int64_t tiles = grid_tiles(n);
   DBuf<unsigned> cnt(tiles, st);
   DBuf<int64_t> toff(tiles, st), tot(1, st);
+  DBuf<int> uns(1, st);
+  int h_uns = 1;
   if (n > 0) {
-    count_nonzero_tiles<<<(int)tiles, CT, 0, st>>>(val, n, cnt.get());
+    CK(cudaMemsetAsync(uns.get(), 0, sizeof(int), st));
+    count_nonzero_tiles<<<(int)tiles, CT, 0, st>>>(val, row1, n, cnt.get(), uns.get());
     CK_LAUNCH();
     note_launch();
     exclusive_scan_u32(st, cnt.get(), tiles, toff.get(), tot.get());
     CK(cudaMemcpyAsync(&c.nkept, tot.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h_uns, uns.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
   const int64_t nk = c.nkept;
@@ -514,8 +513,10 @@ ConvLocal convert_local(cudaStream_t st, const int64_t* row1, const int64_t* col
   note_launch();
   const uint64_t max_key = (uint64_t)(nrb * ncb - 1);
   bool in_tmp = false;
-  // nrb a power of two: row-sorted input needs only the block-column bits
-  const int low = (nrb & (nrb - 1)) == 0 ? key_bits((uint64_t)(nrb - 1)) : 0;
+  // rows non-decreasing and nrb a power of two: the keys (br + nrb bc) are
+  // then non-decreasing in their low log2(nrb) bits, only the block-column
+  // bits need sorting
+  const int low = (!h_uns && (nrb & (nrb - 1)) == 0) ? key_bits((uint64_t)(nrb - 1)) : 0;
   radix_sort_pairs(st, key.get(), pos.get(), nk, key_bits(max_key), key2.get(), pos2.get(), in_tmp,
                    low);
   const uint64_t* sk = in_tmp ? key2.get() : key.get();
