@@ -15,5 +15,6 @@ from .rsvd import (DEFAULT_ROUND_TOL, LowRankSvd, merge_leading_cores, mpo_matmu
                    mpo_svd, reconstruct_matrix, subspace_iteration, tnrsvd)
 from .sparse import (ConversionResult, SparseMatrixCoo, convert_structure, matrix_to_mpo,
                      min_rank_lower_bound)
+from .io import load_mpo, read_matrix_market, save_mpo, write_matrix_market
 
 __version__ = "0.1.0"

@@ -63,6 +63,11 @@ class SparseMatrixCoo:
         r, c = np.nonzero(arr)
         return cls(arr.shape[0], arr.shape[1], r + 1, c + 1, arr[r, c])
 
+    def to_scipy(self):
+        import scipy.sparse as sp
+        return sp.coo_matrix((self.val, (self.row - 1, self.col - 1)),
+                             shape=(self.rows, self.cols))
+
     def to_dense(self) -> np.ndarray:
         out = np.zeros((self.rows, self.cols))
         out[self.row - 1, self.col - 1] = self.val

@@ -230,8 +230,24 @@ def big():
     print("c4", coo.val.size, m.ranks[1])
 
 
+def io_fixtures():
+    """Reference-written .mpo and Matrix Market files (byte-compatibility
+    fixtures for paper_1707_07803_b200.io)."""
+    m = rmpo.random_mpo([2, 3, 2], [2, 2, 3], [3, 4], seed=18)
+    rmpo.save_mpo(m, os.path.join(HERE, "io_ref.mpo"))
+    rng = np.random.default_rng(7)
+    dense = np.where(rng.random((9, 13)) < 0.2, rng.standard_normal((9, 13)), 0.0)
+    coo = rsparse.SparseMatrixCoo.from_dense(dense)
+    rsparse.write_matrix_market(os.path.join(HERE, "io_ref.mtx"), coo)
+    np.savez_compressed(os.path.join(HERE, "io_ref_mtx.npz"), rows=np.array(coo.rows),
+                        cols=np.array(coo.cols), row=coo.row, col=coo.col, val=coo.val)
+    print("io fixtures written")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "--big":
         big()
+    elif len(sys.argv) > 1 and sys.argv[1] == "--io":
+        io_fixtures()
     else:
         main()
