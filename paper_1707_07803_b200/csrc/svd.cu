@@ -368,10 +368,16 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     jq[i] = row == NPR + jw ? 1.0 : 0.0;
   }
   EIG_T(3)
+#ifdef MPO_EIG_PROF
+  long long ph[4] = {0, 0, 0, 0};
+#endif
   for (int sweep = 0; sweep < a.inner; ++sweep) {
     int any = 0;
     for (int r = 0; r < nrounds; ++r) {
       const int par = r & 1;
+#ifdef MPO_EIG_PROF
+      long long q0 = clock64();
+#endif
       if (t < NPR) {
         const int p = a.cross ? t : s_pq[r][t][0];
         const int q = a.cross ? NPR + (t + r) % NPR : s_pq[r][t][1];
@@ -409,7 +415,13 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
         rdq[t] = fma(s * s, gpp, fma(2.0 * c * s, gpq, c * c * gqq));
         any |= rot;
       }
+#ifdef MPO_EIG_PROF
+      long long q1 = clock64();
+#endif
       __syncthreads();
+#ifdef MPO_EIG_PROF
+      long long q2 = clock64();
+#endif
       const double *rcp = rc[r], *rsp = rs[r];
 #pragma unroll
       for (int b = 0; b < BPT; ++b) {
@@ -439,6 +451,9 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
         G[a10] = su * x00 + cu * x10;
         G[a11] = su * x01 + cu * x11;
       }
+#ifdef MPO_EIG_PROF
+      long long q3 = clock64();
+#endif
       if (a.cross) {
         const double c = rcp[jw], sn = rsp[jw];
 #pragma unroll
@@ -448,7 +463,17 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
           jq[i] = __shfl_sync(0xffffffffu, sn * x + c * y, jsrc);
         }
       }
+#ifdef MPO_EIG_PROF
+      long long q4 = clock64();
+#endif
       __syncthreads();
+#ifdef MPO_EIG_PROF
+      long long q5 = clock64();
+      ph[0] += q1 - q0; ph[1] += q2 - q1; ph[2] += q3 - q2; ph[3] += q4 - q3;
+      if (r == nrounds - 1 && pair == 0 && (t == 0 || t == 100) && (g_eig_launch % 97) == 5 && g_eig_launch < 2000)
+        printf("  t=%d per round: rot %lld syncA %lld upd %lld J %lld syncB(last) %lld\n", t,
+               ph[0] / nrounds, ph[1] / nrounds, ph[2] / nrounds, ph[3] / nrounds, q5 - q4);
+#endif
     }
     EIG_T(4)
     if (a.cross) {
