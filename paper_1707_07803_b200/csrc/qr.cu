@@ -256,7 +256,12 @@ struct ClusterPanelArgs {
   double* tau;
 };
 
-__global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPanelArgs p) {
+// cluster panel threads: 16 warps; the dot phase splits each 4-column group's
+// rows over QRC / 256 warps, the rank-1 update gives every thread <= 1 row of
+// a 512-row CTA slice
+constexpr int QRC = 512;
+constexpr int QRC_H = QRC / 256;   // row halves per column group in the dot phase
+__global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs p) {
   extern __shared__ double chunk[];  // rpc x w, column-major
   __shared__ double s_pub[2][2 * QR_NB];   // published partials (dots | row jj), by parity
   __shared__ double s_tot[2 * QR_NB];
@@ -264,6 +269,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
   __shared__ double s_vtv[QR_NB * QR_NB];
   __shared__ double s_tau[QR_NB];
   __shared__ double s_red[16 * 2 * QR_NB];
+  __shared__ double s_dpart[QRC_H][QR_NB];
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks(), c = (int)cluster.block_rank();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
   const int64_t r0 = (int64_t)c * p.rpc;
   const int64_t rem = p.mp - r0;
   const int nr = rem <= 0 ? 0 : (int)(rem < p.rpc ? rem : p.rpc);
-  for (int idx = t; idx < nr * w; idx += QR_THREADS) {
+  for (int idx = t; idx < nr * w; idx += QRC) {
     int r = idx % nr, col = idx / nr;
     chunk[r + col * ld] = p.A[(r0 + r) + col * p.lda];
   }
@@ -286,34 +292,43 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
   for (int jj = 0; jj < w; ++jj) {
     const int ncols = w - jj;            // slot 0: column jj itself (its norm)
     double* pub = s_pub[jj & 1];
-    for (int col0 = warp * 4; col0 < ncols; col0 += QR_THREADS / 8) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int r = lane; r < nr; r += 32) {
-        if (r0 + r > jj) {
-          const double x = chunk[r + jj * ld];
+    {
+      const int grp = warp % 8, half = warp / 8, col0 = grp * 4;
+      if (col0 < ncols) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int r = lane + 32 * half; r < nr; r += 32 * QRC_H) {
+          if (r0 + r > jj) {
+            const double x = chunk[r + jj * ld];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (col0 + u < ncols) acc[u] = fma(x, chunk[r + (jj + col0 + u) * ld], acc[u]);
+            for (int u = 0; u < 4; ++u)
+              if (col0 + u < ncols) acc[u] = fma(x, chunk[r + (jj + col0 + u) * ld], acc[u]);
+          }
         }
-      }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double sum = warp_sum(acc[u]);
-        if (lane == 0 && col0 + u < ncols) pub[col0 + u] = sum;
+        for (int u = 0; u < 4; ++u) {
+          const double sum = warp_sum(acc[u]);
+          if (lane == 0 && col0 + u < ncols) s_dpart[half][col0 + u] = sum;
+        }
       }
     }
     const bool owner = jj >= r0 && jj < r0 + nr;
-    for (int u = t; u < ncols; u += QR_THREADS)
+    __syncthreads();
+    for (int u = t; u < ncols; u += QRC) {
+      double d = 0.0;
+#pragma unroll
+      for (int h = 0; h < QRC_H; ++h) d += s_dpart[h][u];
+      pub[u] = d;
       pub[QR_NB + u] = owner ? chunk[(jj - r0) + (jj + u) * ld] : 0.0;
+    }
     cluster.sync();
     // gather every rank's partials concurrently, then sum in rank order
-    for (int idx = t; idx < CS * 2 * ncols; idx += QR_THREADS) {
+    for (int idx = t; idx < CS * 2 * ncols; idx += QRC) {
       const int rk = idx / (2 * ncols), e = idx % (2 * ncols);
       const int slot = e < ncols ? e : QR_NB + (e - ncols);
       s_red[rk * 2 * QR_NB + slot] = cluster.map_shared_rank(pub, rk)[slot];
     }
     __syncthreads();
-    for (int e = t; e < 2 * ncols; e += QR_THREADS) {
+    for (int e = t; e < 2 * ncols; e += QRC) {
       const int slot = e < ncols ? e : QR_NB + (e - ncols);
       double tot = 0.0;
       for (int i = 0; i < CS; ++i) tot += s_red[i * 2 * QR_NB + slot];
@@ -330,11 +345,11 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
       scal = 1.0 / (al - beta);
     }
     if (t == 0) s_tau[jj] = tau;
-    for (int c = 1 + t; c < ncols; c += QR_THREADS)
+    for (int c = 1 + t; c < ncols; c += QRC)
       s_w[c] = tau * fma(scal, s_tot[c], s_tot[QR_NB + c]);
     __syncthreads();
     // v = [1; scal x]; rank-1 update of the later panel columns
-    for (int r = t; r < nr; r += QR_THREADS) {
+    for (int r = t; r < nr; r += QRC) {
       const int64_t gr = r0 + r;
       if (gr < jj) continue;
       double* rowp = chunk + r + jj * ld;
@@ -345,7 +360,7 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
     }
     __syncthreads();
   }
-  for (int idx = t; idx < nr * w; idx += QR_THREADS) {
+  for (int idx = t; idx < nr * w; idx += QRC) {
     int r = idx % nr, col = idx / nr;
     int64_t gr = r0 + r;
     double x = chunk[r + col * ld];
@@ -355,11 +370,11 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_cluster_kernel(ClusterPan
     chunk[r + col * ld] = v;
   }
   __syncthreads();
-  vtv_partial_dmma(chunk, ld, nr, w, s_vtv);
+  if (warp < 8) vtv_partial_dmma(chunk, ld, nr, w, s_vtv);
   cluster.sync();
   if (c == 0) {
     // sum the V^T V partials (fixed rank order) in place, then dlarft
-    for (int idx = t; idx < w * w; idx += QR_THREADS) {
+    for (int idx = t; idx < w * w; idx += QRC) {
       double tot = 0.0;
       double xv[16];   // all remote loads in flight, then the rank-order sum
 #pragma unroll
@@ -450,7 +465,7 @@ static void factor_panel(cudaStream_t st, double* A, int64_t lda, int64_t mp, in
     ClusterPanelArgs ca{A, lda, mp, w, (int)crpc, V, ldv, T, tau};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CS);
-    cfg.blockDim = dim3(QR_THREADS);
+    cfg.blockDim = dim3(QRC);
     cfg.dynamicSmemBytes = csmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
