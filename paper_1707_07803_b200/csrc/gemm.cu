@@ -7,6 +7,13 @@
 // (rsvd.py:108, :136), the blocked-Householder trailing updates that replace
 // LAPACK dgeqrf/dorgqr (rsvd.py:106, :132, :160), the Jacobi SVD's Q*V
 // back-transform (rsvd.py:128) and the leading-core merge (rsvd.py:95).
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -202,10 +209,43 @@ __global__ void splitk_reduce(const double* __restrict__ W, int nsplit, int64_t 
 
 }  // namespace
 
+namespace {
+// MPO_B200_GEMM_STATS=1: per-shape call counts and flops, printed at exit
+// (diagnostics: which GEMM shapes the sweeps spend their DGEMM time on)
+struct GemmStats {
+  std::mutex mu;
+  std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int, int>, int64_t> calls;
+  ~GemmStats() {
+    if (calls.empty()) return;
+    std::vector<std::pair<double, std::string>> rows;
+    for (auto& kv : calls) {
+      auto [m, n, k, b, ta, tb] = kv.first;
+      const double f = 2.0 * m * n * k * b * kv.second;
+      char buf[160];
+      snprintf(buf, sizeof(buf), "gemm %c%c m=%lld n=%lld k=%lld batch=%lld calls=%lld gflop=%.2f",
+               ta ? 'T' : 'N', tb ? 'T' : 'N', (long long)m, (long long)n, (long long)k,
+               (long long)b, (long long)kv.second, f / 1e9);
+      rows.emplace_back(f, buf);
+    }
+    std::sort(rows.begin(), rows.end(), [](auto& x, auto& y) { return x.first > y.first; });
+    for (size_t i = 0; i < rows.size() && i < 40; ++i) fprintf(stderr, "[mpo_b200] %s\n", rows[i].second.c_str());
+  }
+};
+GemmStats& gemm_stats() {
+  static GemmStats g;
+  return g;
+}
+}  // namespace
+
 void dgemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
            const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
            int64_t ldc, int64_t batch, int64_t sA, int64_t sB, int64_t sC) {
   if (m <= 0 || n <= 0 || batch <= 0) return;
+  static const bool stats = std::getenv("MPO_B200_GEMM_STATS") != nullptr;
+  if (stats) {
+    std::lock_guard<std::mutex> lk(gemm_stats().mu);
+    gemm_stats().calls[{m, n, k, batch, (int)ta, (int)tb}] += 1;
+  }
   if (k <= 0) {
     scale_matrix(st, m, n, beta, C, ldc, batch, sC);
     return;
