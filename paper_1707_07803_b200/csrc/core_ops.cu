@@ -470,6 +470,7 @@ SideStream& side_stream(cudaStream_t main) {
   int lo = 0, hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   CK(cudaStreamCreateWithPriority(&x.hp, cudaStreamNonBlocking, hi));
+  CK(cudaStreamCreateWithPriority(&x.aux, cudaStreamNonBlocking, hi));
   for (auto& e : x.e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   cache.push_back(x);
   return cache.back();

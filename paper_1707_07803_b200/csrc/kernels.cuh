@@ -93,6 +93,7 @@ void core0_finish(cudaStream_t st, const double* in, int64_t I1, int64_t K, int6
 struct SideStream {
   cudaStream_t main = nullptr, sv = nullptr;
   cudaStream_t hp = nullptr;   // highest-priority stream (latency-critical chains)
+  cudaStream_t aux = nullptr;  // highest-priority helper (QR: compact-WY T assembly)
   cudaEvent_t e[8] = {};
 };
 SideStream& side_stream(cudaStream_t main);

@@ -519,7 +519,11 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
   const int gmax = 148;
   DBuf<double> part(gmax, st), wpart((size_t)gmax * QR_NB, st),
       vtv((size_t)gmax * QR_NB * QR_NB, st), alpha(1, st);
-  DBuf<double> Tp((size_t)QR_NB * QR_NB, st), S((size_t)NBO * NBO, st), tmp((size_t)NBO * QR_NB, st);
+  // one compact-WY T slot per inner panel of an outer block (indexed by the
+  // panel's first column): the outer T is assembled on the aux stream while
+  // the panel chain moves on, so a panel's T must outlive the next panels
+  DBuf<double> TpAll((size_t)NBO * QR_NB * QR_NB, st), S((size_t)NBO * NBO, st),
+      tmp((size_t)NBO * QR_NB, st);
   DBuf<double> W, W2;
   // look-ahead (see the trailing update below) for matrices with > 2 outer blocks
   static const bool lookahead = std::getenv("MPO_B200_QR_LOOKAHEAD")
@@ -528,6 +532,9 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
   const bool la = lookahead && nob > 2 && n > 2 * NBO;
   SideStream* sd = la ? &side_stream(st) : nullptr;
   cudaEvent_t ev_panel = la ? sd->e[4] : nullptr, ev_far = la ? sd->e[5] : nullptr;
+  cudaEvent_t ev_v = la ? sd->e[6] : nullptr, ev_t = la ? sd->e[7] : nullptr;
+  // the outer-T assembly (off the panel chain's critical path) runs here
+  cudaStream_t ts = la ? sd->aux : st;
   // the panel chain (panels, in-block updates, near updates) runs on the
   // highest-priority stream so its small launches are scheduled ahead of
   // the far updates' CTAs
@@ -540,6 +547,7 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
     CK(cudaEventRecord(ev_panel, st));              // A, V, T initialised
     CK(cudaStreamWaitEvent(sd->sv, ev_panel, 0));
     CK(cudaStreamWaitEvent(ps, ev_panel, 0));
+    CK(cudaStreamWaitEvent(ts, ev_panel, 0));
     Ws.alloc((size_t)NBO * n, sd->sv);
     Ws2.alloc((size_t)NBO * n, sd->sv);
   }
@@ -550,16 +558,20 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
     for (int64_t i0 = 0, wi = 0; i0 < wo; i0 += wi) {
       const int64_t jj = j0 + i0, mpi = m - jj;
       wi = std::min<int64_t>(panel_width(mpi, QR_NB), wo - i0);
-      factor_panel(ps, A + jj + jj * lda, lda, mpi, wi, Vo + i0 + i0 * mp, mp, Tp.get(),
+      double* Tpi = TpAll.get() + i0 * QR_NB * QR_NB;
+      factor_panel(ps, A + jj + jj * lda, lda, mpi, wi, Vo + i0 + i0 * mp, mp, Tpi,
                    tau.get() + jj, part.get(), wpart.get(), vtv.get(), alpha.get());
-      // place the panel's T on the diagonal of the outer T
-      copy_matrix(ps, wi, wi, Tp.get(), wi, To + i0 + i0 * wo, wo);
+      if (la) {
+        CK(cudaEventRecord(ev_v, ps));
+        CK(cudaStreamWaitEvent(ts, ev_v, 0));
+      }
+      // place the panel's T on the diagonal of the outer T (aux stream)
+      copy_matrix(ts, wi, wi, Tpi, wi, To + i0 + i0 * wo, wo);
       if (i0 > 0) {
         // To[0:i0, i0:i0+wi] = -To[0:i0, 0:i0] (V[:, 0:i0]^T V[:, i0:i0+wi]) Tp
-        dgemm(ps, true, false, i0, wi, mp, 1.0, Vo, mp, Vo + i0 * mp, mp, 0.0, S.get(), i0);
-        dgemm(ps, false, false, i0, wi, i0, 1.0, To, wo, S.get(), i0, 0.0, tmp.get(), i0);
-        dgemm(ps, false, false, i0, wi, wi, -1.0, tmp.get(), i0, Tp.get(), wi, 0.0,
-              To + i0 * wo, wo);
+        dgemm(ts, true, false, i0, wi, mp, 1.0, Vo, mp, Vo + i0 * mp, mp, 0.0, S.get(), i0);
+        dgemm(ts, false, false, i0, wi, i0, 1.0, To, wo, S.get(), i0, 0.0, tmp.get(), i0);
+        dgemm(ts, false, false, i0, wi, wi, -1.0, tmp.get(), i0, Tpi, wi, 0.0, To + i0 * wo, wo);
       }
       // update the rest of this outer block with the panel's reflectors
       const int64_t rem = wo - (i0 + wi);
@@ -568,7 +580,7 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
         const double* Vi = Vo + i0 + i0 * mp;
         ensure(wi * rem);
         dgemm(ps, true, false, wi, rem, mpi, 1.0, Vi, mp, Ar, lda, 0.0, W.get(), wi);
-        dgemm(ps, true, false, wi, rem, wi, 1.0, Tp.get(), wi, W.get(), wi, 0.0, W2.get(), wi);
+        dgemm(ps, true, false, wi, rem, wi, 1.0, Tpi, wi, W.get(), wi, 0.0, W2.get(), wi);
         dgemm(ps, false, false, mpi, rem, wi, -1.0, Vi, mp, W2.get(), wi, 1.0, Ar, lda);
       }
     }
@@ -578,6 +590,10 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
     // stream and overlap the next block's latency-bound panels (<= 16 SMs).
     // Main waits for far(b-1) before near(b): the near columns were part of
     // far(b-1)'s range.
+    if (la) {   // the outer T of this block is assembled
+      CK(cudaEventRecord(ev_t, ts));
+      CK(cudaStreamWaitEvent(ps, ev_t, 0));
+    }
     const int64_t nt = n - (j0 + wo);
     if (nt > 0) {
       const int64_t near = la ? std::min<int64_t>(nt, NBO) : nt, far = nt - near;
