@@ -48,7 +48,7 @@ struct JK {
   static constexpr int GLD = P2 + 1;       // Gram / J row stride in the eig kernel
   static constexpr int NSEG = P2 * 32 / 2; // 16-byte segments per 32-row chunk
 #ifndef MPO_EIG_ET64
-#define MPO_EIG_ET64 512
+#define MPO_EIG_ET64 1024
 #endif
 #ifndef MPO_EIG_ET32
 #define MPO_EIG_ET32 256
@@ -371,6 +371,134 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
 #ifdef MPO_EIG_PROF
   long long ph[4] = {0, 0, 0, 0};
 #endif
+  if (a.cross) {
+    // Cross-block schedule, register-resident (ET == NPR^2): thread (u, v)
+    // owns the 2x2 block of pairs (u, v) of the current round --
+    //   ga = G[p_u][p_v], gc = G[p_u][q_v], gt = G[q_u][p_v], gb = G[q_u][q_v]
+    // with p_w = w, q_w = NPR + (w + r) mod NPR -- and updates it in
+    // registers.  Advancing the round moves q_w to q_{w+1}: gc comes from
+    // the next lane (shuffle), gt and gb from the next row of threads
+    // (one shared-memory exchange).  Thread (w, w) owns pair w's plane and
+    // computes its rotation from its own registers.  J rows {u, u + NPR}
+    // are held in registers the same way (columns p_v, q_v).
+    static_assert(ET == NPR * NPR, "cross-mode eig needs NPR^2 threads");
+    const int u = t / NPR, v = t % NPR, un = (u + 1) % NPR, vn = (v + 1) % NPR;
+    auto gidx = [&](int x, int y) { return min(x, y) * GLD + max(x, y); };
+    double ga = G[gidx(u, v)], gc = G[gidx(u, NPR + v)], gt = G[gidx(NPR + u, v)],
+           gb = G[gidx(NPR + u, NPR + v)];
+    double jp0 = (u == v) ? 1.0 : 0.0, jq0 = 0.0;              // J[u][p_v], J[u][q_v]
+    double jp1 = 0.0, jq1 = (u == v) ? 1.0 : 0.0;              // J[u+NPR][p_v], J[u+NPR][q_v]
+    __shared__ double xrc[NPR], xrs[NPR], xg[3][NPR];
+    __shared__ int xrf[NPR];
+    __syncthreads();   // G is read into registers; its space becomes the exchange buffer
+    double* xt = G;                       // [NPR][NPR + 1]
+    double* xb = G + NPR * (NPR + 1);     // [NPR][NPR + 1]
+    int any = 0;
+#ifdef MPO_EIG_PROF
+    long long xq[4] = {0, 0, 0, 0};
+#endif
+    for (int sweep = 0; sweep < a.inner; ++sweep) {
+      for (int r = 0; r < NPR; ++r) {
+#ifdef MPO_EIG_PROF
+        long long z0 = clock64();
+#endif
+        // the pair planes' entries go to warp 0, which computes all NPR
+        // rotations lane-parallel (FP64 issue slots are per warp
+        // instruction: one warp, not NPR warps with one live lane each)
+        if (u == v) { xg[0][u] = ga; xg[1][u] = gb; xg[2][u] = gc; }
+        __syncthreads();
+        if (t < NPR) {
+          const double gpp = xg[0][t], gqq = xg[1][t], gpq = xg[2][t];
+          const double pq = gpp * gqq;
+          const bool rot = gpp > 0.0 && gqq > 0.0 && gpq * gpq > gfl * fmax(gpp, gqq) &&
+                           (pq > 1e-280 ? gpq * gpq > a.tol * a.tol * pq
+                                        : fabs(gpq) * rsqrt(gpp) * rsqrt(gqq) > a.tol);
+          double c = 1.0, sn = 0.0;
+          if (rot) {
+            const double d = gqq - gpp, g2 = 2.0 * fabs(gpq);
+            const double mx = fmax(fabs(d), g2);
+            float df, gf;
+            if (mx > 1e-18 && mx < 1e18) {
+              df = (float)fabs(d);
+              gf = (float)g2;
+            } else {
+              const double sc = scalbn(1.0, -ilogb(mx));
+              df = (float)(fabs(d) * sc);
+              gf = (float)(g2 * sc);
+            }
+            const float r2 = fmaf(df, df, gf * gf);
+            const float tf = __fdividef(gf, df + r2 * rsqrtf(r2));
+            const float cf = rsqrtf(fmaf(tf, tf, 1.0f));
+            const double sg = (d == 0.0) ? 1.0 : ((d > 0.0) == (gpq > 0.0) ? 1.0 : -1.0);
+            c = (double)cf;
+            sn = sg * (double)tf * (double)cf;
+            const double f = 1.5 - 0.5 * fma(c, c, sn * sn);
+            c *= f;
+            sn *= f;
+            any = 1;
+          }
+          xrc[t] = c;
+          xrs[t] = sn;
+          xrf[t] = rot;
+          xg[0][t] = fma(c * c, gpp, fma(-2.0 * c * sn, gpq, sn * sn * gqq));
+          xg[1][t] = fma(sn * sn, gpp, fma(2.0 * c * sn, gpq, c * c * gqq));
+        }
+#ifdef MPO_EIG_PROF
+        long long z1 = clock64();
+#endif
+        __syncthreads();
+#ifdef MPO_EIG_PROF
+        long long z2 = clock64();
+#endif
+        const double cu = xrc[u], su = xrs[u], cv = xrc[v], sv = xrs[v];
+        if (u == v) {
+          if (xrf[u]) { ga = xg[0][u]; gb = xg[1][u]; gc = 0.0; gt = 0.0; }
+        } else {
+          // R_u^T [[ga, gc], [gt, gb]] R_v
+          const double x00 = cv * ga - sv * gc, x01 = sv * ga + cv * gc;
+          const double x10 = cv * gt - sv * gb, x11 = sv * gt + cv * gb;
+          ga = cu * x00 - su * x10;
+          gc = cu * x01 - su * x11;
+          gt = su * x00 + cu * x10;
+          gb = su * x01 + cu * x11;
+        }
+        {  // J rows u, u + NPR: columns p_v, q_v rotated by rotation v
+          const double a0 = jp0, b0 = jq0, a1 = jp1, b1 = jq1;
+          jp0 = cv * a0 - sv * b0;
+          jq0 = sv * a0 + cv * b0;
+          jp1 = cv * a1 - sv * b1;
+          jq1 = sv * a1 + cv * b1;
+        }
+        // advance to round r+1: q_v <- q_{v+1}
+        gc = __shfl_sync(0xffffffffu, gc, vn, NPR);
+        jq0 = __shfl_sync(0xffffffffu, jq0, vn, NPR);
+        jq1 = __shfl_sync(0xffffffffu, jq1, vn, NPR);
+        xt[u * (NPR + 1) + v] = gt;
+        xb[u * (NPR + 1) + v] = gb;
+#ifdef MPO_EIG_PROF
+        long long z3 = clock64();
+#endif
+        __syncthreads();
+        gt = xt[un * (NPR + 1) + v];
+        gb = xb[un * (NPR + 1) + vn];
+#ifdef MPO_EIG_PROF
+        long long z4 = clock64();
+        xq[0] += z1 - z0; xq[1] += z2 - z1; xq[2] += z3 - z2; xq[3] += z4 - z3;
+        if (r == NPR - 1 && pair == 0 && (t == 0 || t == 1 || t == 33) && (g_eig_launch % 97) == 5 && g_eig_launch < 2000)
+          printf("  reg t=%d per round: rot %lld sync1 %lld upd+shfl %lld sync2+ld %lld\n", t, xq[0] / NPR,
+                 xq[1] / NPR, xq[2] / NPR, xq[3] / NPR);
+#endif
+      }
+    }
+    EIG_T(4)
+    // after NPR rounds per sweep every q_w is back at NPR + w
+    J[u * GLD + v] = jp0;
+    J[u * GLD + NPR + v] = jq0;
+    J[(u + NPR) * GLD + v] = jp1;
+    J[(u + NPR) * GLD + NPR + v] = jq1;
+    EIG_T(5)
+    __syncthreads_or(any);
+  } else {
   for (int sweep = 0; sweep < a.inner; ++sweep) {
     int any = 0;
     for (int r = 0; r < nrounds; ++r) {
@@ -489,6 +617,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     }
     EIG_T(5)
     if (!__syncthreads_or(any)) break;
+  }
   }
   // re-orthogonalise J: two Newton-Schulz steps J <- J - J (J^T J - I) / 2
   // (each squares the orthogonality defect of the accumulated rotations),
