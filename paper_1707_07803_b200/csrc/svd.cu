@@ -242,17 +242,23 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
 #endif
   EIG_T(0)
   {
-    // sum the row-split partial Grams in split order (loads issued first)
+    // sum the row-split partial Grams in split order (loads issued first);
+    // only the upper triangle is formed by the gram kernel and read here
     constexpr int PER = P2 * P2 / ET;
     const double* gp = a.gpart + (int64_t)pair * a.splits * (P2 * P2) + t;
     double sacc[PER];
+    bool up[PER];
 #pragma unroll
-    for (int e = 0; e < PER; ++e) sacc[e] = 0.0;
+    for (int e = 0; e < PER; ++e) {
+      sacc[e] = 0.0;
+      const int idx = t + e * ET;
+      up[e] = idx / P2 <= idx % P2;
+    }
 #pragma unroll 4
     for (int sp = 0; sp < a.splits; ++sp) {
       double v[PER];
 #pragma unroll
-      for (int e = 0; e < PER; ++e) v[e] = gp[(int64_t)sp * P2 * P2 + e * ET];
+      for (int e = 0; e < PER; ++e) v[e] = up[e] ? gp[(int64_t)sp * P2 * P2 + e * ET] : 0.0;
 #pragma unroll
       for (int e = 0; e < PER; ++e) sacc[e] += v[e];
     }
@@ -268,12 +274,16 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
   __syncthreads();   // only the upper triangle of G is read from here on
   const double gfl = a.floorc * (*a.fro) * (*a.fro);   // (c eps ||X||_F)^2
   {
+    // column norms once (sqrt before multiplying: G_ii * G_jj underflows for
+    // graded columns)
+    __shared__ double s_nrm[P2];
+    for (int i = t; i < P2; i += ET) s_nrm[i] = sqrt(G[i * GLD + i]);
+    __syncthreads();
     bool rot = false;
     for (int idx = t; idx < P2 * P2; idx += ET) {
       int i = idx / P2, j = idx % P2;
       if (i < j) {
-        // sqrt before multiplying: G_ii * G_jj underflows for graded columns
-        double d = sqrt(G[i * GLD + i]) * sqrt(G[j * GLD + j]);
+        double d = s_nrm[i] * s_nrm[j];
         const double g = fabs(G[i * GLD + j]);
         if (d > 0.0 && g > a.tol * d &&
             g * g > gfl * fmax(G[i * GLD + i], G[j * GLD + j]))
