@@ -1100,8 +1100,15 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   splits = (int)cdiv(kp, rps);
   DBuf<double> gpart((size_t)npairs * splits * P2 * P2, st), J((size_t)npairs * P2 * P2, st);
   DBuf<int> skip(npairs, st), flag(1, st);
-  static const int inner =
-      std::getenv("MPO_B200_INNER") ? std::atoi(std::getenv("MPO_B200_INNER")) : 1;
+  // inner sweeps of each pair's Gram: two for large k, where the eig runs
+  // hidden behind the side-stream V update and a better-converged pair
+  // saves outer sweeps (13 -> 11 at k = 4096), one for small k, where the
+  // eig latency is exposed
+  static const int inner_env =
+      std::getenv("MPO_B200_INNER") ? std::atoi(std::getenv("MPO_B200_INNER")) : 0;
+  static const int64_t inner2_mink =
+      std::getenv("MPO_B200_INNER2_MINK") ? std::atoll(std::getenv("MPO_B200_INNER2_MINK")) : 3072;
+  const int inner = inner_env > 0 ? inner_env : (k >= inner2_mink ? 2 : 1);
   // one step suffices: every rotation is orthogonal to O(eps) (FP64
   // renormalised), so J's defect after one inner sweep is ~P2 eps and one
   // quadratic step takes it to rounding level
