@@ -1109,6 +1109,9 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   static const int64_t inner2_mink =
       std::getenv("MPO_B200_INNER2_MINK") ? std::atoll(std::getenv("MPO_B200_INNER2_MINK")) : 3072;
   const int inner = inner_env > 0 ? inner_env : (k >= inner2_mink ? 2 : 1);
+  // ... in the first sweeps only (later sweeps are near convergence)
+  static const int inner_sweeps =
+      std::getenv("MPO_B200_INNER_SWEEPS") ? std::atoi(std::getenv("MPO_B200_INNER_SWEEPS")) : 1000;
   // one step suffices: every rotation is orthogonal to O(eps) (FP64
   // renormalised), so J's defect after one inner sweep is ~P2 eps and one
   // quadratic step takes it to rounding level
@@ -1309,6 +1312,7 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
       const int par = (int)(rr & 1);
       a.round = r;
       a.cross = cross_from >= 0 && sweep >= cross_from && r > 0;
+      a.inner = sweep < inner_sweeps ? inner : 1;
       a.J = Jb[par];
       a.skip = Sb[par];
       if (prof) CK(cudaEventRecord(ev[4 * r], st));
