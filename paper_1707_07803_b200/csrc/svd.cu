@@ -363,20 +363,6 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     bu[b] = idx < NBLK ? s_blk[idx][0] : -1;
     bv[b] = idx < NBLK ? s_blk[idx][1] : -1;
   }
-  // cross-block schedule (rounds r: p = w, q = NPR + (w + r) mod NPR): J is
-  // held in registers -- lane w of a warp owns J[row][p_w] and J[row][q_w]
-  // for RPL rows, applies rotation w, and the q side moves one lane per
-  // round (q_w of round r+1 is q_{w+1} of round r): no shared-memory traffic
-  constexpr int NWJ = ET / 32, RW = P2 / NWJ, LPR = 32 / NPR, RPL = RW / LPR;
-  const int jw = lane % NPR, jrow0 = warp * RW + lane / NPR;
-  const int jsrc = (lane / NPR) * NPR + (jw + 1) % NPR;
-  double jp[RPL], jq[RPL];
-#pragma unroll
-  for (int i = 0; i < RPL; ++i) {
-    const int row = jrow0 + i * LPR;
-    jp[i] = row == jw ? 1.0 : 0.0;
-    jq[i] = row == NPR + jw ? 1.0 : 0.0;
-  }
   EIG_T(3)
 #ifdef MPO_EIG_PROF
   long long ph[4] = {0, 0, 0, 0};
@@ -517,8 +503,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
       long long q0 = clock64();
 #endif
       if (t < NPR) {
-        const int p = a.cross ? t : s_pq[r][t][0];
-        const int q = a.cross ? NPR + (t + r) % NPR : s_pq[r][t][1];
+        const int p = s_pq[r][t][0], q = s_pq[r][t][1];
         const double gpp = G[p * GLD + p], gqq = G[q * GLD + q], gpq = G[p * GLD + q];
         const double pq = gpp * gqq;
         const bool rot = gpp > 0.0 && gqq > 0.0 && gpq * gpq > gfl * fmax(gpp, gqq) &&
@@ -565,8 +550,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
       for (int b = 0; b < BPT; ++b) {
         const int u = bu[b], v = bv[b];
         if (u < 0) continue;
-        const int pu = a.cross ? u : s_pq[r][u][0];
-        const int qu = a.cross ? NPR + (u + r) % NPR : s_pq[r][u][1];
+        const int pu = s_pq[r][u][0], qu = s_pq[r][u][1];
         if (u == v) {
           if (!rflag[par][u]) continue;   // a non-rotating pair keeps its g_pq
           G[pu * GLD + pu] = rdp[u];
@@ -575,8 +559,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
           continue;
         }
         // (c, s) = (1, 0) for a non-rotating pair: the update is then exact
-        const int pv = a.cross ? v : s_pq[r][v][0];
-        const int qv = a.cross ? NPR + (v + r) % NPR : s_pq[r][v][1];
+        const int pv = s_pq[r][v][0], qv = s_pq[r][v][1];
         const double cu = rcp[u], su = rsp[u], cv = rcp[v], sv = rsp[v];
         // entry (a, b) of the symmetric G lives at min(a,b)*GLD + max(a,b)
         const int a00 = min(pu, pv) * GLD + max(pu, pv), a01 = min(pu, qv) * GLD + max(pu, qv);
@@ -590,19 +573,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
         G[a11] = su * x01 + cu * x11;
       }
 #ifdef MPO_EIG_PROF
-      long long q3 = clock64();
-#endif
-      if (a.cross) {
-        const double c = rcp[jw], sn = rsp[jw];
-#pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const double x = jp[i], y = jq[i];
-          jp[i] = c * x - sn * y;
-          jq[i] = __shfl_sync(0xffffffffu, sn * x + c * y, jsrc);
-        }
-      }
-#ifdef MPO_EIG_PROF
-      long long q4 = clock64();
+      long long q3 = clock64(), q4 = q3;
 #endif
       __syncthreads();
 #ifdef MPO_EIG_PROF
@@ -614,17 +585,7 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
 #endif
     }
     EIG_T(4)
-    if (a.cross) {
-      // after NPR rounds the q side is back at q_w = NPR + w
-#pragma unroll
-      for (int i = 0; i < RPL; ++i) {
-        const int row = jrow0 + i * LPR;
-        J[row * GLD + jw] = jp[i];
-        J[row * GLD + NPR + jw] = jq[i];
-      }
-    } else {
-      j_accumulate(nrounds);
-    }
+    j_accumulate(nrounds);
     EIG_T(5)
     if (!__syncthreads_or(any)) break;
   }
