@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--no-conversion", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-batched", action="store_true")
+    p.add_argument("--no-c3", action="store_true")
     return p.parse_args()
 
 
@@ -372,6 +373,8 @@ def run_b200(args, rank, world, local_rank):
     if not args.no_conversion:
         line["conversion"] = bench_conversion(args, torch, dist, rank, world, dev, barrier,
                                               max_over_ranks)
+    if not args.no_c3:
+        line["tnrsvd_c3q0"] = bench_c3q0(args, torch, rank, world, barrier, max_over_ranks)
     if not args.no_batched:
         line["tnrsvd_batched"] = bench_batched(args, torch, rank, world, barrier, max_over_ranks,
                                                cfg="c5inst")
@@ -388,6 +391,38 @@ def run_b200(args, rank, world, local_rank):
                                                   "seconds": cs}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def bench_c3q0(args, torch, rank, world, barrier, max_over_ranks):
+    """Config 3 (d=12, n=4, rank 64, decaying middle bond; K=32, p=16) at
+    q=0, the largest setting the reference finishes (213 s on 8 cores in
+    the build container; q=2 needs a 1.5 TiB product core at rsvd.py:77).
+    One replica per rank, device-resident inputs, CUDA-event timed."""
+    from paper_1707_07803_b200.rsvd import prepare, tnrsvd_prepared
+    from paper_1707_07803_b200.workloads import TNRSVD_ARGS, config_mpo
+    kw = TNRSVD_ARGS["c3q0"]
+    am, o, _ = prepare(config_mpo("c3q0"), kw["k_target"], kw["oversample"], kw["seed"])
+    tnrsvd_prepared(am, o, kw["k_target"], kw["q"], kw["round_tol"])   # warm-up
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = 2
+    e0.record()
+    for _ in range(steps):
+        _, s, _ = tnrsvd_prepared(am, o, kw["k_target"], kw["q"], kw["round_tol"])
+    e1.record()
+    e1.synchronize()
+    secs = max_over_ranks(e0.elapsed_time(e1) / 1e3 / steps)
+    try:
+        flops = ledger_flops("c3q0")
+    except (KeyError, OSError, ValueError):
+        flops = None
+    return {"metric": "config-3 TNrSVD (q=0) time-to-K-triplets", "seconds": secs,
+            "value": (flops / secs / 1e12 * world) if flops else None, "unit": "TFLOP/s",
+            "ledger_flops_per_step": flops, "n_gpus": world, "scaling": "weak",
+            "reference_seconds_build_container": 213.2, "s_head": [float(x) for x in s[:3]],
+            "note": "q=0: the BASELINE q=2 is infeasible for the reference and for any faithful "
+                    "implementation (exact bond ranks 16384 at rank-64x16384 products)"}
 
 
 def bench_batched(args, torch, rank, world, barrier, max_over_ranks, n_inst=64, threads=8,
