@@ -28,6 +28,7 @@
 // fixed reduction orders: bitwise deterministic.
 #include <chrono>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -127,6 +128,7 @@ struct JacArgs {
   double* J;       // npairs * P2*P2 (row-major)
   int* skip;       // npairs
   int* flag;       // any rotation in this sweep
+  unsigned* cmax;  // largest significant relative coupling this sweep (float bits)
   double tol;
   const double* fro;  // ||X||_F (device scalar; invariant under rotations)
   double floorc;      // pairs with g_pq^2 <= floorc ||X||_F^2 max(g_pp, g_qq) are noise
@@ -280,15 +282,22 @@ __global__ void __launch_bounds__(JK<JB>::ET) jacobi_eig_kernel(JacArgs a) {
     for (int i = t; i < P2; i += ET) s_nrm[i] = sqrt(G[i * GLD + i]);
     __syncthreads();
     bool rot = false;
+    float cm = 0.f;   // largest relative coupling above the noise floor
     for (int idx = t; idx < P2 * P2; idx += ET) {
       int i = idx / P2, j = idx % P2;
       if (i < j) {
         double d = s_nrm[i] * s_nrm[j];
         const double g = fabs(G[i * GLD + j]);
-        if (d > 0.0 && g > a.tol * d &&
-            g * g > gfl * fmax(G[i * GLD + i], G[j * GLD + j]))
-          rot = true;
+        if (d > 0.0 && g * g > gfl * fmax(G[i * GLD + i], G[j * GLD + j])) {
+          cm = fmaxf(cm, (float)(g / d));
+          if (g > a.tol * d) rot = true;
+        }
       }
+    }
+    if (a.cmax) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+      if (lane == 0 && cm > 0.f) atomicMax(a.cmax, __float_as_uint(cm));
     }
     if (__syncthreads_or(rot)) s_skip = 0;
   }
@@ -1080,6 +1089,8 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   // use cross-block-only inner sweeps (-1: never)
   static const int cross_from =
       std::getenv("MPO_B200_CROSS_FROM") ? std::atoi(std::getenv("MPO_B200_CROSS_FROM")) : 0;
+  static const double trunc_stop =
+      std::getenv("MPO_B200_TRUNC_STOP") ? std::atof(std::getenv("MPO_B200_TRUNC_STOP")) : 1e-5;
   static const int ns_steps =
       std::getenv("MPO_B200_NS") ? std::atoi(std::getenv("MPO_B200_NS")) : 1;
   // J and skip flags are double-buffered by round parity: the V updates of
@@ -1099,7 +1110,8 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
       std::getenv("MPO_B200_JFLOOR") ? std::atof(std::getenv("MPO_B200_JFLOOR")) : 1.0;
   DBuf<double> fro(1, st);
   frob_norm(st, X, kp * kp, fro.get());
-  JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), Jb[0], Sb[0], flag.get(), tol,
+  DBuf<unsigned> cmaxb(1, st);
+  JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), Jb[0], Sb[0], flag.get(), cmaxb.get(), tol,
             fro.get(), noise_floor ? floor_mult * floor_mult * eps * eps : 0.0, inner, ns_steps,
             nullptr, 0, 0, nullptr, nullptr};
   // profiling (bench.py roofline): CUDA events around every round kernel;
@@ -1269,6 +1281,7 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
       }
     }
     CK(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
+    CK(cudaMemsetAsync(cmaxb.get(), 0, sizeof(unsigned), st));
     for (int r = 0; r < nb - 1; ++r, ++rr) {
       const int par = (int)(rr & 1);
       a.round = r;
@@ -1296,7 +1309,9 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
       if (prof) CK(cudaEventRecord(ev[4 * r + 3], st));
     }
     note_launch(4 * (nb - 1));
+    unsigned h_cmax = 0;
     CK(cudaMemcpyAsync(&h_flag, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&h_cmax, cmaxb.get(), sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (trace_lvl >= 2) {
       std::vector<int> sk((size_t)(nb - 1) * npairs);
@@ -1324,6 +1339,14 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
     }
     ++sweeps;
     if (!h_flag) break;
+    // truncation SVDs (noise_floor): once a whole sweep's couplings were all
+    // below trunc_stop, the next sweep would leave O(trunc_stop^2) ones --
+    // the column norms are then singular values to O(trunc_stop^2) relative,
+    // and V, and so the exact factorisation X0 = X V^T, is orthogonal
+    // regardless of convergence: stop without the confirming sweep
+    float cm_f;
+    memcpy(&cm_f, &h_cmax, sizeof(float));
+    if (noise_floor && trunc_stop > 0.0 && cm_f <= trunc_stop) break;
   }
   if (overlap) {
     // the main stream continues only after the last V update
