@@ -53,6 +53,17 @@ void core_product(cudaStream_t st, const CoreView& a, const CoreView& b, double*
 // explicitly; replaces np.linalg.qr(mode="reduced") (LAPACK dgeqrf+dorgqr).
 void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda, double* Q,
                     int64_t ldq, double* R, int64_t ldr);
+// The same factorisation keeping the compact-WY reflectors (no explicit Q),
+// and C <- Q C for an m x ncols matrix C (qr.cu).
+struct QrReflectors {
+  static constexpr int NBO = 128;   // outer block width
+  int64_t m = 0, k = 0;
+  std::vector<int64_t> voff, wos;
+  DBuf<double> V, T;
+};
+void householder_qr_keep(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda,
+                         double* R, int64_t ldr, QrReflectors& f);
+void qr_apply_q(cudaStream_t st, const QrReflectors& f, double* C, int64_t ldc, int64_t ncols);
 
 // Thin SVD of a column-major m x n matrix (svd.cu).  Returns all min(m,n)
 // singular values (descending, on the device) and the column-sorted

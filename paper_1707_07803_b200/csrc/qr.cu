@@ -498,9 +498,10 @@ static void factor_panel(cudaStream_t st, double* A, int64_t lda, int64_t mp, in
 // updated once per outer block with K = 128 DMMA GEMMs (compute-bound rather
 // than one rank-32 HBM pass per panel).  The outer block's T is assembled
 // from the panels' T's: T = [[T1, -T1 (V1^T V2) T2], [0, T2]].
-void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda, double* Q,
-                    int64_t ldq, double* R, int64_t ldr) {
-  constexpr int NBO = 128;
+static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda,
+                                double* Q, int64_t ldq, double* R, int64_t ldr,
+                                QrReflectors* keep) {
+  constexpr int NBO = QrReflectors::NBO;
   const int64_t k = std::min(m, n);
   if (k <= 0) return;
   const int64_t nob = cdiv(k, NBO);
@@ -629,18 +630,56 @@ void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t ld
     CK_LAUNCH();
     note_launch();
   }
+  if (keep) {
+    keep->m = m;
+    keep->k = k;
+    keep->voff = voff;
+    keep->wos = wos;
+    keep->V = std::move(V);
+    keep->T = std::move(T);
+  }
   if (!Q) return;
-  // dorgqr: Q = H_1 ... H_k [I; 0], outer blocks applied last to first
+  // dorgqr: Q = H_1 ... H_k [I; 0], outer blocks applied last to first (a
+  // block's reflectors act only on rows j0.. and, for [I; 0], on columns j0..)
   set_identity(st, m, k, Q, ldq);
   for (int64_t b = nob - 1; b >= 0; --b) {
     const int64_t j0 = b * NBO, wo = wos[b], mp = m - j0, nq = k - j0;
-    double* Vo = V.get() + voff[b];
-    double* To = T.get() + b * NBO * NBO;
+    const double* Vo = (keep ? keep->V.get() : V.get()) + voff[b];
+    const double* To = (keep ? keep->T.get() : T.get()) + b * NBO * NBO;
     double* Qb = Q + j0 + j0 * ldq;
     ensure(wo * nq);
     dgemm(st, true, false, wo, nq, mp, 1.0, Vo, mp, Qb, ldq, 0.0, W.get(), wo);
     dgemm(st, false, false, wo, nq, wo, 1.0, To, wo, W.get(), wo, 0.0, W2.get(), wo);
     dgemm(st, false, false, mp, nq, wo, -1.0, Vo, mp, W2.get(), wo, 1.0, Qb, ldq);
+  }
+}
+
+void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda, double* Q,
+                    int64_t ldq, double* R, int64_t ldr) {
+  householder_qr_impl(st, m, n, A, lda, Q, ldq, R, ldr, nullptr);
+}
+
+void householder_qr_keep(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda,
+                         double* R, int64_t ldr, QrReflectors& f) {
+  householder_qr_impl(st, m, n, A, lda, nullptr, 0, R, ldr, &f);
+}
+
+// C <- Q C for the m x ncols matrix C (Q = H_1 ... H_k from householder_qr_keep):
+// the dorgqr recurrence on an arbitrary right-hand side, so Q times a
+// k-column block costs one reflector sweep instead of forming Q and a GEMM
+void qr_apply_q(cudaStream_t st, const QrReflectors& f, double* C, int64_t ldc, int64_t ncols) {
+  constexpr int NBO = QrReflectors::NBO;
+  const int64_t nob = (int64_t)f.wos.size();
+  if (ncols <= 0 || nob == 0) return;
+  DBuf<double> W((size_t)NBO * ncols, st), W2((size_t)NBO * ncols, st);
+  for (int64_t b = nob - 1; b >= 0; --b) {
+    const int64_t j0 = b * NBO, wo = f.wos[b], mp = f.m - j0;
+    const double* Vo = f.V.get() + f.voff[b];
+    const double* To = f.T.get() + b * NBO * NBO;
+    double* Cb = C + j0;
+    dgemm(st, true, false, wo, ncols, mp, 1.0, Vo, mp, Cb, ldc, 0.0, W.get(), wo);
+    dgemm(st, false, false, wo, ncols, wo, 1.0, To, wo, W.get(), wo, 0.0, W2.get(), wo);
+    dgemm(st, false, false, mp, ncols, wo, -1.0, Vo, mp, W2.get(), wo, 1.0, Cb, ldc);
   }
 }
 

@@ -1390,7 +1390,11 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   auto tq = std::chrono::steady_clock::now();
   const bool wide = m <= n;            // factor M^T = Q T  (n x m, tall)
   const int64_t tm = wide ? n : m;     // tall orientation rows
-  DBuf<double> A((size_t)tm * k, st), Q((size_t)tm * k, st), R((size_t)k * k, st);
+  DBuf<double> A((size_t)tm * k, st), R((size_t)k * k, st);
+  // Q is never formed: the finishing products Q Ys / Q Vs apply the kept
+  // reflectors to [Ys; 0] / [Vs; 0] (the dorgqr recurrence on k columns),
+  // which saves a tm x k x k GEMM per SVD
+  QrReflectors f1, f2;
   if (wide) {
     int64_t dims[2] = {m, n};
     int perm[2] = {1, 0};
@@ -1403,7 +1407,7 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   } else {
     copy_matrix(st, m, n, M, ldm, A.get(), m);
   }
-  householder_qr(st, tm, k, A.get(), tm, Q.get(), tm, R.get(), k);
+  householder_qr_keep(st, tm, k, A.get(), tm, R.get(), k, f1);
   // Tall M = Q T: one more (k x k) QR, T^T = Q2 T2, so that the Jacobi runs
   // on the lower-triangular T2^T (T = T2^T Q2^T).  One-sided Jacobi converges
   // much faster on the transposed triangular factor (Drmac & Veselic, the
@@ -1412,14 +1416,12 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   static const bool tall_lq =
       std::getenv("MPO_B200_TALL_LQ") ? std::atoi(std::getenv("MPO_B200_TALL_LQ")) != 0 : true;
   const bool lq = !wide && tall_lq;
-  DBuf<double> Q2;
   if (lq) {
     DBuf<double> A2((size_t)k * k, st);
     int64_t dims[2] = {k, k};
     int pr[2] = {1, 0};
     permute(st, R.get(), A2.get(), 2, dims, pr);
-    Q2.alloc((size_t)k * k, st);
-    householder_qr(st, k, k, A2.get(), k, Q2.get(), k, R.get(), k);
+    householder_qr_keep(st, k, k, A2.get(), k, R.get(), k, f2);
   }
   // X = T^T (wide, or tall with the second QR) or T (tall), zero padded to kp x kp
   DBuf<double> X((size_t)kp * kp, st), V((size_t)kp * kp, st);
@@ -1472,20 +1474,33 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
     fprintf(stderr, "[mpo_b200]   outalloc %lldx%lld %.3f ms\n", (long long)m, (long long)n, ms);
     ta = std::chrono::steady_clock::now();
   }
+  // [B; 0] (rows x k) -> Q_f [B; 0] in place
+  auto apply_q = [&](const QrReflectors& f, const double* B, int64_t rows, double* C,
+                     int64_t ldc) {
+    fill_zero(st, C, ldc * k);
+    copy_matrix(st, k, k, B, k, C, ldc);
+    qr_apply_q(st, f, C, ldc, k);
+    (void)rows;
+  };
+  int64_t dkk[2] = {k, k};
+  int pr[2] = {1, 0};
   if (wide) {
-    // M = X Q^T, X Vs = Ys:  Ucarry = Ys (m = k rows),  Vh = Vs^T Q^T = (Q Vs)^T
+    // M = X Q^T, X Vs = Ys:  Ucarry = Ys (m = k rows),  Vh = (Q Vs)^T
     copy_matrix(st, k, k, Ys.get(), k, out.ucarry.get(), m);
-    dgemm(st, true, true, k, n, k, 1.0, Vs.get(), k, Q.get(), tm, 0.0, out.vh.get(), k);
+    DBuf<double> QV((size_t)tm * k, st);
+    apply_q(f1, Vs.get(), tm, QV.get(), tm);
+    int64_t dims[2] = {tm, k};
+    permute(st, QV.get(), out.vh.get(), 2, dims, pr);
   } else if (lq) {
     // M = Q X Q2^T:  Ucarry = Q Ys,  Vh = (Q2 Vs)^T
-    dgemm(st, false, false, m, k, k, 1.0, Q.get(), tm, Ys.get(), k, 0.0, out.ucarry.get(), m);
-    dgemm(st, true, true, k, k, k, 1.0, Vs.get(), k, Q2.get(), k, 0.0, out.vh.get(), k);
+    apply_q(f1, Ys.get(), m, out.ucarry.get(), m);
+    DBuf<double> QV((size_t)k * k, st);
+    apply_q(f2, Vs.get(), k, QV.get(), k);
+    permute(st, QV.get(), out.vh.get(), 2, dkk, pr);
   } else {
     // M = Q X:  Ucarry = Q Ys,  Vh = Vs^T
-    dgemm(st, false, false, m, k, k, 1.0, Q.get(), tm, Ys.get(), k, 0.0, out.ucarry.get(), m);
-    int64_t dims[2] = {k, k};
-    int pr[2] = {1, 0};
-    permute(st, Vs.get(), out.vh.get(), 2, dims, pr);
+    apply_q(f1, Ys.get(), m, out.ucarry.get(), m);
+    permute(st, Vs.get(), out.vh.get(), 2, dkk, pr);
   }
   if (trace) {
     CK(cudaStreamSynchronize(st));
