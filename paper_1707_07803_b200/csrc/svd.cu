@@ -668,7 +668,8 @@ __global__ void __launch_bounds__(JT, 2) jacobi_apply_kernel(JacArgs a) {
   const int pair = blockIdx.x;
   if (a.skip[pair]) return;
   const int split = blockIdx.y;
-  double* M = a.which == 0 ? a.X : a.V;
+  // which: 0 = X, 1 = V, 2 = both (blockIdx.z picks; one launch for small problems)
+  double* M = (a.which == 2 ? (int)blockIdx.z : a.which) == 0 ? a.X : a.V;
   int bx, by;
   pair_of_round(a.nb, a.round, pair, bx, by);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1132,7 +1133,11 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   }
   cudaStream_t sv = st;
   cudaEvent_t evE[2] = {nullptr, nullptr}, evV[2] = {nullptr, nullptr};
-  const bool overlap = !prof && npairs >= 16;   // large problems only
+  static const int combined_max =
+      std::getenv("MPO_B200_APPLY_COMBINED_MAXPAIRS")
+          ? std::atoi(std::getenv("MPO_B200_APPLY_COMBINED_MAXPAIRS")) : 32;
+  const bool combined = !prof && npairs <= combined_max;
+  const bool overlap = !prof && !combined && npairs >= 16;   // large problems only
   if (overlap) {
     SideStream* sd = &side_stream(st);   // cached per (host thread, main stream)
     sv = sd->sv;
@@ -1298,14 +1303,21 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
       CK_LAUNCH();
       if (prof) CK(cudaEventRecord(ev[4 * r + 2], st));
       if (overlap) CK(cudaEventRecord(evE[par], st));
-      a.which = 0;
-      jacobi_apply_kernel<JB><<<dim3(npairs, splits), JT, apply_smem<JB>(), st>>>(a);
-      CK_LAUNCH();
-      a.which = 1;
-      if (overlap) CK(cudaStreamWaitEvent(sv, evE[par], 0));
-      jacobi_apply_kernel<JB><<<dim3(npairs, splits), JT, apply_smem<JB>(), sv>>>(a);
-      CK_LAUNCH();
-      if (overlap) CK(cudaEventRecord(evV[par], sv));
+      if (combined) {
+        // small problems: X and V in one launch on the main stream
+        a.which = 2;
+        jacobi_apply_kernel<JB><<<dim3(npairs, splits, 2), JT, apply_smem<JB>(), st>>>(a);
+        CK_LAUNCH();
+      } else {
+        a.which = 0;
+        jacobi_apply_kernel<JB><<<dim3(npairs, splits), JT, apply_smem<JB>(), st>>>(a);
+        CK_LAUNCH();
+        a.which = 1;
+        if (overlap) CK(cudaStreamWaitEvent(sv, evE[par], 0));
+        jacobi_apply_kernel<JB><<<dim3(npairs, splits), JT, apply_smem<JB>(), sv>>>(a);
+        CK_LAUNCH();
+        if (overlap) CK(cudaEventRecord(evV[par], sv));
+      }
       if (prof) CK(cudaEventRecord(ev[4 * r + 3], st));
     }
     note_launch(4 * (nb - 1));
