@@ -1064,8 +1064,11 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   // row splits: npairs * splits <= 592 = one wave of the gram kernel (4 CTAs
   // per SM) and two waves of the apply kernel (2 per SM); rounding up would
   // leave a nearly empty tail wave
-  static const int wave =
-      std::getenv("MPO_B200_JWAVE") ? std::atoi(std::getenv("MPO_B200_JWAVE")) : 592;
+  // (16-column blocks, k <= 1024: one CTA per SM -- fewer, longer splits
+  // cut the eig's partial-Gram reduction, which dominates there)
+  static const int wave_env =
+      std::getenv("MPO_B200_JWAVE") ? std::atoi(std::getenv("MPO_B200_JWAVE")) : 0;
+  const int wave = wave_env > 0 ? wave_env : (JB == 16 ? 148 : 592);
   int splits = (int)std::min<int64_t>(std::max<int64_t>(1, wave / npairs), cdiv(kp, CH));
   int64_t rps = cdiv(cdiv(kp, splits), CH) * CH;
   splits = (int)cdiv(kp, rps);
