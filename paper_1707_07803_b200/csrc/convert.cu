@@ -6,15 +6,18 @@
 //      coordinate (i1 = r % I1, br = r / I1; same for columns,
 //      sparse.py:240-242) and key the block column-block-major
 //      (key = br + nrb * bc, sparse.py:245-246);
-//   2. stable LSD radix sort of (key, position), 8-bit digits, only the
-//      bits the key space needs;
+//   2. stable onesweep LSD radix sort of (key, position), 8-bit digits,
+//      only the bits the key space needs (only the block-column bits when
+//      the rows arrive non-decreasing);
 //   3. segment: head flags -> block ids (np.unique's return_inverse,
 //      sparse.py:247), sorted unique keys, ti scattered back to input order.
 //
 // HBM-bound integer work: no tensor cores, coalesced tile loads, grids in
-// multiples of the SM count, and no atomics anywhere (per-warp private
-// shared-memory counters driven by __match_any_sync + popc, prefix sums
-// over tiles in a fixed order), so the output is bit-deterministic.
+// multiples of the SM count.  Ranks come from per-warp private shared-memory
+// counters driven by __match_any_sync + popc and prefix sums in a fixed
+// order; the few atomics (histogram counts, tile-id dispenser, decoupled
+// look-back flags, the sortedness flag) compute order-independent values,
+// so the output is bit-deterministic.
 #include "common.cuh"
 #include "convert.cuh"
 #include "kernels.cuh"
