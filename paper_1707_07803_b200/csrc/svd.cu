@@ -1094,7 +1094,7 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   static const int cross_from =
       std::getenv("MPO_B200_CROSS_FROM") ? std::atoi(std::getenv("MPO_B200_CROSS_FROM")) : 0;
   static const double trunc_stop =
-      std::getenv("MPO_B200_TRUNC_STOP") ? std::atof(std::getenv("MPO_B200_TRUNC_STOP")) : 1e-5;
+      std::getenv("MPO_B200_TRUNC_STOP") ? std::atof(std::getenv("MPO_B200_TRUNC_STOP")) : 1e-4;
   static const int ns_steps =
       std::getenv("MPO_B200_NS") ? std::atoi(std::getenv("MPO_B200_NS")) : 1;
   // J and skip flags are double-buffered by round parity: the V updates of
