@@ -110,6 +110,10 @@ int mpo_conv_level(mpo_ctx* ctx, const mpo_conv* c, int level, int64_t* row_digi
 /* dense core `level` (0..d-1) of the summed unit-rank terms (sparse.py:183-204
  * densified as Mpo.densify, mpo.py:184-197) */
 int mpo_conv_dense_core(mpo_ctx* ctx, const mpo_conv* c, int level, double* dst, int to_host);
+/* device MPO of the unit-rank terms of blocks [start, stop), dense cores
+ * (one chunk of the capped accumulation, sparse.py:260-271) */
+int mpo_conv_chunk(mpo_ctx* ctx, const mpo_conv* c, int64_t start, int64_t stop,
+                   mpo_dev** out);
 int mpo_conv_free(mpo_conv* c);
 
 /* ---- multi-GPU conversion merge helpers (no reference counterpart: the
@@ -120,6 +124,11 @@ int mpo_keys_unique(mpo_ctx* ctx, const int64_t* keys, int64_t n, int64_t max_ke
 /* out[i] = index of q[i] in the sorted table (binary search; -1 if absent) */
 int mpo_keys_lookup(mpo_ctx* ctx, const int64_t* table, int64_t ntab, const int64_t* q,
                     int64_t nq, int64_t* out);
+/* out[i] = offset + lower_bound(table, q[i]) over the sorted table; with
+ * exact != 0, -1 where q[i] is absent (device in/out).  Splitter positions
+ * and range-local -> global block ids of the key-range exchange. */
+int mpo_keys_search(mpo_ctx* ctx, const int64_t* table, int64_t ntab, const int64_t* q,
+                    int64_t nq, int64_t offset, int exact, int64_t* out);
 /* ti[i] = map[ti[i]] in place (device) */
 int mpo_remap_ids(mpo_ctx* ctx, const int64_t* map, int64_t* ti, int64_t n);
 

@@ -438,6 +438,56 @@ def conversion_structure(row1, col1, val, row_factors, col_factors):
                                val[keep], uniq.astype(np.int64), int(uniq.size))
 
 
+def coo_validate(rows, cols, row1, col1, val):
+    """SparseMatrixCoo.__init__ checks (sparse.py:53-70): lengths, 1-based
+    ranges and the duplicate-coordinate rejection (np.unique of the keys).
+    CPU-baseline port of the constructor bench.py times separately."""
+    row1 = np.asarray(row1, dtype=np.int64).reshape(-1)
+    col1 = np.asarray(col1, dtype=np.int64).reshape(-1)
+    val = np.asarray(val, dtype=np.float64).reshape(-1)
+    if not (row1.size == col1.size == val.size):
+        raise ValueError("row/col/val arrays must have equal length")
+    if row1.size:
+        if row1.min() < 1 or row1.max() > rows:
+            raise ValueError("row index out of range")
+        if col1.min() < 1 or col1.max() > cols:
+            raise ValueError("col index out of range")
+        keys = (row1 - 1) * cols + (col1 - 1)
+        if np.unique(keys).size != keys.size:
+            raise ValueError("duplicate (row, col) entries rejected")
+    return row1, col1, val
+
+
+def matrix_to_mpo_arrays(row1, col1, val, row_factors, col_factors):
+    """The whole uncapped matrix_to_mpo with sparse cores
+    (sparse.py:207-258 + _build_cores :183-204), as parallel index arrays
+    per core (left, row, col, right, values): the same numpy work the
+    reference does, including its per-nonzero level digits (:243-244), whose
+    results it never uses.  CPU-baseline port (bench.py)."""
+    keep = val != 0
+    r0 = row1[keep] - 1
+    c0 = col1[keep] - 1
+    values = val[keep]
+    i1_, j1_ = int(row_factors[0]), int(col_factors[0])
+    i1, br = r0 % i1_, r0 // i1_
+    j1, bc = c0 % j1_, c0 // j1_
+    digits(br, row_factors[1:])          # sparse.py:243-244 (dead in the reference too)
+    digits(bc, col_factors[1:])
+    nrb = math.prod(int(f) for f in row_factors[1:])
+    key = br + nrb * bc
+    uniq, ti = np.unique(key, return_inverse=True)
+    rank = uniq.size
+    u_row = digits(uniq % nrb, row_factors[1:])
+    u_col = digits(uniq // nrb, col_factors[1:])
+    d = len(row_factors)
+    cores = [(np.zeros_like(ti), i1, j1, ti, values)]
+    t = np.arange(rank, dtype=np.int64)
+    ones = np.ones(rank)
+    for k in range(1, d):
+        cores.append((t, u_row[k - 1], u_col[k - 1], t if k < d - 1 else np.zeros_like(t), ones))
+    return cores
+
+
 def block_digits(uniq, row_factors, col_factors):
     """u_row / u_col of sparse.py:249-250."""
     nrb = math.prod(int(f) for f in row_factors[1:])

@@ -57,9 +57,11 @@ SIGNATURES = {
     "mpo_conv_copy": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, C.c_int]),
     "mpo_conv_level": (C.c_int, [_P, _P, C.c_int, _P, _P, C.c_int]),
     "mpo_conv_dense_core": (C.c_int, [_P, _P, C.c_int, _P, C.c_int]),
+    "mpo_conv_chunk": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.POINTER(_P)]),
     "mpo_conv_free": (C.c_int, [_P]),
     "mpo_keys_unique": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, _I64P]),
     "mpo_keys_lookup": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P]),
+    "mpo_keys_search": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int64, C.c_int, _P]),
     "mpo_remap_ids": (C.c_int, [_P, _P, _P, C.c_int64]),
 }
 

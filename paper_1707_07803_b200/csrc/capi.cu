@@ -349,6 +349,24 @@ MPO_API int mpo_conv_level(mpo_ctx* ctx, const mpo_conv* c, int level, int64_t* 
   });
 }
 
+MPO_API int mpo_conv_chunk(mpo_ctx* ctx, const mpo_conv* c, int64_t start, int64_t stop,
+                           mpo_dev** out) {
+  return guarded(ctx, [&] {
+    need(start >= 0 && stop > start && stop <= c->c.rank, "chunk out of range");
+    const int d = (int)c->rf.size();
+    const int64_t sub = stop - start;
+    mpob::Cores cs;
+    for (int k = 0; k < d; ++k) {
+      mpob::Core core = k == 0 ? mpob::make_core(ctx->stream, 1, c->rf[0], c->cf[0], sub)
+                               : mpob::make_core(ctx->stream, sub, c->rf[k], c->cf[k],
+                                                 k == d - 1 ? 1 : sub);
+      mpob::conv_chunk_core(ctx->stream, c->c, c->rf, c->cf, k, start, stop, core.p());
+      cs.push_back(std::move(core));
+    }
+    *out = wrap(std::move(cs));
+  });
+}
+
 MPO_API int mpo_conv_dense_core(mpo_ctx* ctx, const mpo_conv* c, int level, double* dst,
                                 int to_host) {
   return guarded(ctx, [&] {
@@ -383,6 +401,11 @@ MPO_API int mpo_keys_unique(mpo_ctx* ctx, const int64_t* keys, int64_t n, int64_
 MPO_API int mpo_keys_lookup(mpo_ctx* ctx, const int64_t* table, int64_t ntab, const int64_t* q,
                             int64_t nq, int64_t* out) {
   return guarded(ctx, [&] { mpob::keys_lookup(ctx->stream, table, ntab, q, nq, out); });
+}
+
+MPO_API int mpo_keys_search(mpo_ctx* ctx, const int64_t* table, int64_t ntab, const int64_t* q,
+                            int64_t nq, int64_t offset, int exact, int64_t* out) {
+  return guarded(ctx, [&] { mpob::keys_search(ctx->stream, table, ntab, q, nq, offset, exact != 0, out); });
 }
 
 MPO_API int mpo_remap_ids(mpo_ctx* ctx, const int64_t* map, int64_t* ti, int64_t n) {

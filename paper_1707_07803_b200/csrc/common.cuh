@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -80,6 +81,20 @@ class DBuf {
 };
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline int current_device() {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  return dev;
+}
+
+// Function attributes (dynamic shared-memory opt-ins) are per device: run a
+// setup once for each device the calling thread targets (thread-safe).
+constexpr int kMaxDevices = 64;
+template <typename F>
+inline void once_per_device(std::once_flag (&flags)[kMaxDevices], F&& fn) {
+  std::call_once(flags[current_device() & (kMaxDevices - 1)], std::forward<F>(fn));
+}
 
 // Count of our own kernel launches (reported by bench.py as gpu_launches).
 extern unsigned long long g_launches;

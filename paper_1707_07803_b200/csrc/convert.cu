@@ -450,12 +450,11 @@ void radix_sort_pairs(cudaStream_t st, uint64_t* key, unsigned* pay, int64_t n, 
   const int npass = (bits - shift0 + 7) / 8;
   if (npass > MAXPASS) throw ValueError("sort key wider than 64 bits");
   const int64_t ntiles = cdiv(n, OS_TILE);
-  static const bool attr = [] {   // thread-safe one-time setup
+  static std::once_flag once[kMaxDevices];   // per device, thread-safe
+  once_per_device(once, [] {
     CK(cudaFuncSetAttribute(onesweep_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)OS_SMEM));
-    return true;
-  }();
-  (void)attr;
+  });
   const int hblk = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, CT * 16), 148 * 4));
   DBuf<unsigned> part((size_t)hblk * npass * RADIX, st), ctr(npass, st);
   DBuf<int64_t> doff((size_t)npass * RADIX, st);

@@ -38,9 +38,16 @@ void radix_sort_pairs(cudaStream_t st, uint64_t* key, unsigned* pay, int64_t n, 
 namespace mpob {
 void conv_dense_core(cudaStream_t st, const ConvLocal& c, const std::vector<int64_t>& rf,
                      const std::vector<int64_t>& cf, int level, double* out);
+// dense core `level` of the unit-rank terms of blocks [start, stop) (one
+// chunk of the capped accumulation, sparse.py:262-271)
+void conv_chunk_core(cudaStream_t st, const ConvLocal& c, const std::vector<int64_t>& rf,
+                     const std::vector<int64_t>& cf, int level, int64_t start, int64_t stop,
+                     double* out);
 int64_t keys_unique(cudaStream_t st, const int64_t* keys, int64_t n, int64_t max_key,
                     int64_t* out);
 void keys_lookup(cudaStream_t st, const int64_t* table, int64_t ntab, const int64_t* q,
                  int64_t nq, int64_t* out);
+void keys_search(cudaStream_t st, const int64_t* table, int64_t ntab, const int64_t* q,
+                 int64_t nq, int64_t offset, bool exact, int64_t* out);
 void remap_ids(cudaStream_t st, const int64_t* map, int64_t* ti, int64_t n);
 }  // namespace mpob

@@ -21,6 +21,16 @@ __global__ void scatter_core0(const int64_t* i1, const int64_t* j1, const int64_
     out[i1[e] + I1 * (j1[e] + J1 * ti[e])] = v[e];   // coordinates are unique: no accumulation
 }
 
+__global__ void scatter_core0_range(const int64_t* i1, const int64_t* j1, const int64_t* ti,
+                                    const double* v, int64_t n, int64_t I1, int64_t J1,
+                                    int64_t start, int64_t stop, double* out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = ti[e];
+    if (t >= start && t < stop) out[i1[e] + I1 * (j1[e] + J1 * (t - start))] = v[e];
+  }
+}
+
 __global__ void scatter_selector(const int64_t* rowd, const int64_t* cold, int64_t rank,
                                  int64_t Ik, int64_t Jk, bool last, double* out) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rank;
@@ -64,6 +74,19 @@ __global__ void lookup_kernel(const int64_t* table, int64_t ntab, const int64_t*
   }
 }
 
+__global__ void search_kernel(const int64_t* table, int64_t ntab, const int64_t* q, int64_t nq,
+                              int64_t offset, bool exact, int64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x = q[i], lo = 0, hi = ntab;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (table[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    out[i] = (exact && !(lo < ntab && table[lo] == x)) ? -1 : lo + offset;
+  }
+}
+
 __global__ void remap_kernel(const int64_t* map, int64_t* ti, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -100,6 +123,34 @@ void conv_dense_core(cudaStream_t st, const ConvLocal& c, const std::vector<int6
   note_launch();
 }
 
+void conv_chunk_core(cudaStream_t st, const ConvLocal& c, const std::vector<int64_t>& rf,
+                     const std::vector<int64_t>& cf, int level, int64_t start, int64_t stop,
+                     double* out) {
+  const int d = (int)rf.size();
+  const int64_t sub = stop - start;
+  int64_t nrb = 1;
+  for (int q = 1; q < d; ++q) nrb *= rf[q];
+  if (level == 0) {
+    fill_zero(st, out, rf[0] * cf[0] * sub);
+    if (c.nkept) {
+      scatter_core0_range<<<gridn(c.nkept), 256, 0, st>>>(c.i1.get(), c.j1.get(), c.ti.get(),
+                                                         c.values.get(), c.nkept, rf[0], cf[0],
+                                                         start, stop, out);
+      CK_LAUNCH();
+      note_launch();
+    }
+    return;
+  }
+  const bool last = level == d - 1;
+  fill_zero(st, out, sub * rf[level] * cf[level] * (last ? 1 : sub));
+  DBuf<int64_t> rd(sub, st), cd(sub, st);
+  level_digits(st, c.uniq.get() + start, sub, nrb, rf, cf, level, rd.get(), cd.get());
+  scatter_selector<<<gridn(sub), 256, 0, st>>>(rd.get(), cd.get(), sub, rf[level], cf[level],
+                                              last, out);
+  CK_LAUNCH();
+  note_launch();
+}
+
 int64_t keys_unique(cudaStream_t st, const int64_t* keys, int64_t n, int64_t max_key,
                     int64_t* out) {
   if (n <= 0) return 0;
@@ -128,6 +179,14 @@ void keys_lookup(cudaStream_t st, const int64_t* table, int64_t ntab, const int6
                  int64_t* out) {
   if (nq <= 0) return;
   lookup_kernel<<<gridn(nq), 256, 0, st>>>(table, ntab, q, nq, out);
+  CK_LAUNCH();
+  note_launch();
+}
+
+void keys_search(cudaStream_t st, const int64_t* table, int64_t ntab, const int64_t* q,
+                 int64_t nq, int64_t offset, bool exact, int64_t* out) {
+  if (nq <= 0) return;
+  search_kernel<<<gridn(nq), 256, 0, st>>>(table, ntab, q, nq, offset, exact, out);
   CK_LAUNCH();
   note_launch();
 }

@@ -461,11 +461,15 @@ void core0_finish(cudaStream_t st, const double* in, int64_t I1, int64_t K, int6
 }
 
 SideStream& side_stream(cudaStream_t main) {
+  // keyed by (device, main stream): the legacy/per-thread default stream has
+  // the same handle on every device, and the side streams belong to one
   thread_local std::deque<SideStream> cache;   // deque: stable references
+  const int dev = current_device();
   for (auto& x : cache)
-    if (x.main == main) return x;
+    if (x.main == main && x.device == dev) return x;
   SideStream x;
   x.main = main;
+  x.device = dev;
   CK(cudaStreamCreateWithFlags(&x.sv, cudaStreamNonBlocking));
   int lo = 0, hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));

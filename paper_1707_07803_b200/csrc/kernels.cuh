@@ -76,12 +76,15 @@ struct SvdOut {
   DBuf<double> vh;      // k x n, column-major, ld = k
   int64_t k = 0;
 };
-// noise_floor: skip rotations whose coupling is below the O(eps ||M||)
-// backward-error level (singular values and the exact product U S Vh are
-// unaffected; U = ucarry / s is then not orthonormal for noise-level s, so
-// callers that need left vectors pass false)
+// trunc_rel > 0 (truncation SVDs): the caller's truncation level delta
+// relative to ||M||_F.  Rotations whose coupling is below a noise floor of
+// min(64 eps, 1e-2 trunc_rel) ||M||_F are skipped (singular values and the
+// exact product U S Vh are unaffected; U = ucarry / s is then not
+// orthonormal for noise-level s, so callers that need left vectors pass 0),
+// and the sweeps may stop early once the couplings are O(1e-4) -- only
+// while the floor sits >= 100x below delta.  0: full convergence.
 void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ldm, SvdOut& out,
-              bool noise_floor = false);
+              double trunc_rel = 0.0);
 
 }  // namespace mpob
 
@@ -103,6 +106,7 @@ void core0_finish(cudaStream_t st, const double* in, int64_t I1, int64_t K, int6
 // Events 0-3 belong to the Jacobi sweeps (svd.cu), 4-7 to the QR (qr.cu).
 struct SideStream {
   cudaStream_t main = nullptr, sv = nullptr;
+  int device = -1;
   cudaStream_t hp = nullptr;   // highest-priority stream (latency-critical chains)
   cudaStream_t aux = nullptr;  // highest-priority helper (QR: compact-WY T assembly)
   cudaEvent_t e[8] = {};

@@ -402,23 +402,27 @@ __global__ void extract_r_kernel(int64_t k, int64_t n, const double* A, int64_t 
 // one-time kernel attribute setup: C++11 magic statics make these
 // thread-safe (the batched path calls in from several host threads)
 int panel_smem_limit() {
-  static const int lim = [] {
-    int dev, l;
-    CK(cudaGetDevice(&dev));
+  static std::once_flag once[kMaxDevices];   // per device (function attributes are)
+  static int lims[kMaxDevices];
+  const int dev = current_device() & (kMaxDevices - 1);
+  std::call_once(once[dev], [dev] {
+    int l;
     CK(cudaDeviceGetAttribute(&l, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, qr_panel_kernel));
     l -= (int)fa.sharedSizeBytes + 1024;
     CK(cudaFuncSetAttribute(qr_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, l));
-    return l;
-  }();
-  return lim;
+    lims[dev] = l;
+  });
+  return lims[dev];
 }
 
 int cluster_smem_limit() {
-  static const int lim = [] {
-    int dev, l;
-    CK(cudaGetDevice(&dev));
+  static std::once_flag once[kMaxDevices];
+  static int lims[kMaxDevices];
+  const int dev = current_device() & (kMaxDevices - 1);
+  std::call_once(once[dev], [dev] {
+    int l;
     CK(cudaDeviceGetAttribute(&l, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, qr_panel_cluster_kernel));
@@ -427,9 +431,9 @@ int cluster_smem_limit() {
                             l));
     CK(cudaFuncSetAttribute(qr_panel_cluster_kernel,
                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    return l;
-  }();
-  return lim;
+    lims[dev] = l;
+  });
+  return lims[dev];
 }
 
 int max_coresident_panel_ctas(size_t smem) {

@@ -1021,24 +1021,22 @@ constexpr size_t apply_smem() {
 }
 
 void sort_smem_attr() {
-  static const bool done = [] {
+  static std::once_flag once[kMaxDevices];
+  once_per_device(once, [] {
     CK(cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             8192 * (int)(sizeof(double) + sizeof(int))));
-    return true;
-  }();
-  (void)done;
+  });
 }
 
 template <int JB>
 void set_smem_attrs() {
-  static const bool done = [] {   // thread-safe one-time setup (magic static)
+  static std::once_flag once[kMaxDevices];   // per device, thread-safe
+  once_per_device(once, [] {
     CK(cudaFuncSetAttribute(jacobi_eig_kernel<JB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)eig_smem<JB>()));
     CK(cudaFuncSetAttribute(jacobi_apply_kernel<JB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)apply_smem<JB>()));
-    return true;
-  }();
-  (void)done;
+  });
 }
 
 }  // namespace
@@ -1049,7 +1047,8 @@ KernelProfile g_prof;
 // and rows >= k are zero).  V (kp x kp) accumulates the rotations.
 template <int JB>
 static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, double* V,
-                         bool noise_floor) {
+                         double trunc_rel) {
+  const bool noise_floor = trunc_rel > 0.0;
   using K = JK<JB>;
   constexpr int P2 = K::P2;
   set_smem_attrs<JB>();
@@ -1115,11 +1114,17 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   // ||A|| / sqrt(d-1) (-1.3 % on the config-2 step vs c = 1)
   static const double floor_mult =
       std::getenv("MPO_B200_JFLOOR") ? std::atof(std::getenv("MPO_B200_JFLOOR")) : 64.0;
+  // ... but never closer than 100x below the caller's truncation level
+  // (mpo_round at rel_tol 1e-14 puts delta below 64 eps ||X||_F): the floor
+  // shrinks with delta, and the early stop below is only taken while the
+  // floor is the full 64 eps (delta >= ~1.4e-12 ||X||_F)
+  const double floor_c = std::min(floor_mult * eps, 1e-2 * trunc_rel);
+  const bool early_stop_ok = noise_floor && floor_c >= floor_mult * eps;
   DBuf<double> fro(1, st);
   frob_norm(st, X, kp * kp, fro.get());
   DBuf<unsigned> cmaxb(1, st);
   JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), Jb[0], Sb[0], flag.get(), cmaxb.get(), tol,
-            fro.get(), noise_floor ? floor_mult * floor_mult * eps * eps : 0.0, inner, ns_steps,
+            fro.get(), noise_floor ? floor_c * floor_c : 0.0, inner, ns_steps,
             nullptr, 0, 0, nullptr, nullptr};
   // profiling (bench.py roofline): CUDA events around every round kernel;
   // the V updates then stay on the main stream so the intervals are exact
@@ -1364,7 +1369,14 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
     // regardless of convergence: stop without the confirming sweep
     float cm_f;
     memcpy(&cm_f, &h_cmax, sizeof(float));
-    if (noise_floor && trunc_stop > 0.0 && cm_f <= trunc_stop) break;
+    if (early_stop_ok && trunc_stop > 0.0 && cm_f <= trunc_stop) { h_flag = 0; break; }
+  }
+  if (h_flag) {
+    // still rotating after 60 sweeps: the column norms are not singular
+    // values and W = ucarry / s would not be orthonormal -- fail loudly
+    for (auto& e : ev) cudaEventDestroy(e);
+    throw std::runtime_error("svd: one-sided Jacobi did not converge in 60 sweeps (k = " +
+                             std::to_string(k) + ")");
   }
   if (overlap) {
     // the main stream continues only after the last V update
@@ -1394,7 +1406,7 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
 }
 
 void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ldm, SvdOut& out,
-              bool noise_floor) {
+              double trunc_rel) {
   const int64_t k = std::min(m, n);
   out.k = k;
   if (k <= 0) return;
@@ -1453,8 +1465,8 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
     fprintf(stderr, "[mpo_b200]   precondition %lldx%lld %.3f ms\n", (long long)m, (long long)n, ms);
   }
   auto t0 = std::chrono::steady_clock::now();
-  const int sweeps = jbw == 16 ? jacobi_sweeps<16>(st, X.get(), k, kp, V.get(), noise_floor)
-                                 : jacobi_sweeps<32>(st, X.get(), k, kp, V.get(), noise_floor);
+  const int sweeps = jbw == 16 ? jacobi_sweeps<16>(st, X.get(), k, kp, V.get(), trunc_rel)
+                                 : jacobi_sweeps<32>(st, X.get(), k, kp, V.get(), trunc_rel);
   if (trace) {
     double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     fprintf(stderr, "[mpo_b200]   jacobi k=%lld sweeps=%d %.3f ms\n", (long long)k, sweeps, ms);

@@ -176,7 +176,9 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
     SvdOut o;
     {
       Trace tr(st, "svd", R, N);
-      svd_thin(st, R, N, c.p(), R, o, /*noise_floor=*/true);
+      // delta relative to this core's norm (= the chain's: the cores left
+      // of k are left-orthonormal, those right of it right-orthonormal)
+      svd_thin(st, R, N, c.p(), R, o, /*trunc_rel=*/tol / std::sqrt((double)(d - 1)));
     }
     std::vector<double> s(o.k);
     CK(cudaMemcpyAsync(s.data(), o.s.get(), sizeof(double) * o.k, cudaMemcpyDeviceToHost, st));

@@ -157,19 +157,61 @@ def convert_structure(row1, col1, val, plan: PartitionPlan, device=None,
     return ConversionResult(h, ctx, plan)
 
 
+class _LevelCore(SparseCore):
+    """Block core k >= 1 of the SparseCore chain (sparse.py:195-203) whose
+    per-block digit arrays (``row``, ``col``) stay on the device until first
+    read: the reference materialises all 2(d-1) of them (10.9 GB at config
+    5), most callers touch none or a few."""
+
+    __slots__ = ("_res", "_k", "_rd", "_cd")
+
+    def __init__(self, shape, left, right, values, res, k):
+        SparseCore.__init__(self, shape, left, _EMPTY, _EMPTY, right, values)
+        self._res, self._k, self._rd, self._cd = res, k, None, None
+
+    def _fetch(self):
+        if self._rd is None:
+            self._rd, self._cd = self._res.level(self._k)
+        return self._rd, self._cd
+
+    @property
+    def row(self):
+        return self._fetch()[0]
+
+    @row.setter
+    def row(self, v):
+        pass
+
+    @property
+    def col(self):
+        return self._fetch()[1]
+
+    @col.setter
+    def col(self, v):
+        pass
+
+    def transpose(self) -> SparseCore:
+        r, i, j, s = self.shape
+        return SparseCore((r, j, i, s), self.left, self.col, self.row, self.right, self.values)
+
+
+_EMPTY = np.zeros(0, dtype=np.int64)
+
+
 def _sparse_cores(res: ConversionResult, i1, j1, ti, values, rank):
     plan = res.plan
     d = plan.d
     cores = [SparseCore((1, plan.row_factors[0], plan.col_factors[0], rank),
                         np.zeros_like(ti), i1, j1, ti, values)]
+    # shared by every block core, as in the reference (sparse.py:194-195)
     t = np.arange(rank, dtype=np.int64)
     ones = np.ones(rank)
+    zero = np.zeros_like(t)
     for k in range(1, d):
-        rd, cd = res.level(k)
         last = k == d - 1
-        cores.append(SparseCore((rank, plan.row_factors[k], plan.col_factors[k],
+        cores.append(_LevelCore((rank, plan.row_factors[k], plan.col_factors[k],
                                  1 if last else rank),
-                                t, rd, cd, np.zeros_like(t) if last else t, ones))
+                                t, zero if last else t, ones, res, k))
     return cores
 
 
@@ -196,26 +238,15 @@ def matrix_to_mpo(a: SparseMatrixCoo, plan: PartitionPlan, rank_cap: int | None 
         i1, j1, ti, values, _ = res.arrays()
         return Mpo(_sparse_cores(res, i1, j1, ti, values, rank))
     # capped accumulation (sparse.py:260-275): chunks of rank_cap unit-rank
-    # terms, densified, stacked with mpo_add and rounded on the device
+    # terms built as dense device cores straight from the conversion handle
+    # (mpo_conv_chunk), stacked with mpo_add and rounded, all on the device
     tol = 1e-14 if round_tol is None else round_tol
-    i1, j1, ti, values, _ = res.arrays()
-    digits = [res.level(k) for k in range(1, d)]
     acc = None
     for start in range(0, rank, rank_cap):
         stop = min(start + rank_cap, rank)
-        pick = np.nonzero((ti >= start) & (ti < stop))[0]
-        sub = stop - start
-        c0 = np.zeros((1, plan.row_factors[0], plan.col_factors[0], sub))
-        np.add.at(c0, (0, i1[pick], j1[pick], ti[pick] - start), values[pick])
-        cores = [c0]
-        t = np.arange(sub)
-        for k in range(1, d):
-            last = k == d - 1
-            c = np.zeros((sub, plan.row_factors[k], plan.col_factors[k], 1 if last else sub))
-            c[t, digits[k - 1][0][start:stop], digits[k - 1][1][start:stop],
-              0 if last else t] = 1.0
-            cores.append(c)
-        chunk = DeviceMpo.from_host(Mpo(cores))
+        h = C.c_void_p()
+        _lib.call("mpo_conv_chunk", res.ctx, res.handle, int(start), int(stop), C.byref(h))
+        chunk = DeviceMpo(h, res.ctx)
         acc = chunk if acc is None else mpo_add(acc, chunk)
         if max(acc.ranks) >= rank_cap:
             acc = mpo_round(acc, tol)

@@ -207,16 +207,72 @@ def big():
     cores = [c / 8.0 for c in a.cores]
     cores[5] = cores[5] * (0.5 ** np.arange(64))[None, None, None, :]
     cases["c3q0"] = (rmpo.Mpo(cores), dict(k_target=32, q=0, round_tol=1e-9, oversample=1.5, seed=4))
-    only = sys.argv[2:] or list(cases)
+    sel = sys.argv[2:]
+    only = [x for x in sel if x in cases] if sel else list(cases)
+    sys.path.insert(0, os.path.dirname(HERE))
+    import mpo_checks as mc   # tests/mpo_checks.py: the same formulas the GPU tests use
     for name in only:
         a, kw = cases[name]
         t0 = time.perf_counter()
         lr = rrsvd.tnrsvd(a, **kw)
         secs = time.perf_counter() - t0
+        # MPO-form accuracy of the reference's own result (BASELINE config 2:
+        # "residual ||A V - U S|| contracted in TT format"), on the merged
+        # operator the factors live on; the 4-layer V^T A^T A V environment
+        # is 4096^2 x 64^2 doubles at config 3, so only U^T A A^T U there
+        am = rrsvd.merge_leading_cores(a, a.num_cores - lr.u.num_cores + 1)
+        t1 = time.perf_counter()
+        chk = mc.summary(lr.u.cores, lr.s, lr.v.cores, am.cores, av=(name != "c3q0"))
+        extra = {f"chk_{k}": np.asarray(v) for k, v in chk.items()}
         np.savez_compressed(os.path.join(HERE, f"big_{name}.npz"), s=lr.s,
                             u_ranks=np.array(lr.u.ranks), v_ranks=np.array(lr.v.ranks),
-                            K=np.array(lr.k_oversampled), seconds=np.array(secs))
-        print(name, secs, lr.u.ranks, lr.v.ranks)
+                            K=np.array(lr.k_oversampled), seconds=np.array(secs), **extra)
+        print(name, secs, time.perf_counter() - t1, lr.u.ranks, lr.v.ranks,
+              chk.get("res_av"), chk.get("res_atu"), flush=True)
+        del lr, am, chk
+    if "conv5" not in sys.argv[2:] and sys.argv[2:]:
+        return
+    conv5()
+    # config 4 conversion (2^16 square band + 1e6 scatter, seed 4)
+    conv4()
+
+
+def _sha(x):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+
+
+def conv5():
+    """Config 5's conversion at full size (2^22 square, power-law rows,
+    seed 55; paper_1707_07803_b200.workloads.powerlaw_coo): the reference's
+    matrix_to_mpo output is kept as sha256 digests of its index arrays (the
+    arrays are ~1 GB), plus the COO constructor and conversion times."""
+    import time
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_1707_07803_b200.workloads import powerlaw_coo
+    n = 1 << 22
+    r, c, v = powerlaw_coo(n, seed=55)
+    t0 = time.perf_counter()
+    coo = rsparse.SparseMatrixCoo(n, n, r, c, v)
+    t_ctor = time.perf_counter() - t0
+    plan = mposvd.plan_partition(n, n, ([2] * 22, [2] * 22))
+    t0 = time.perf_counter()
+    m = rsparse.matrix_to_mpo(coo, plan, densify_limit=0)
+    t_conv = time.perf_counter() - t0
+    c0 = m.cores[0]
+    lv = [1, 11, 21]
+    out = dict(nnz=np.array(c0.values.size), rank=np.array(m.ranks[1]),
+               ti_sha=np.array(_sha(c0.right)), i1_sha=np.array(_sha(c0.row)),
+               j1_sha=np.array(_sha(c0.col)), values_sha=np.array(_sha(c0.values)),
+               levels=np.array(lv),
+               lvl_row_sha=np.array([_sha(m.cores[k].row) for k in lv]),
+               lvl_col_sha=np.array([_sha(m.cores[k].col) for k in lv]),
+               seconds_ctor=np.array(t_ctor), seconds_convert=np.array(t_conv))
+    np.savez_compressed(os.path.join(HERE, "big_c5conv.npz"), **out)
+    print("c5conv", out["nnz"], out["rank"], t_ctor, t_conv, flush=True)
+
+
+def conv4():
     # config 4 conversion (2^16 square band + 1e6 scatter, seed 4)
     coo = band_scatter(1 << 16, 1_000_000, seed=4)
     plan = mposvd.plan_partition(1 << 16, 1 << 16, ([2] * 16, [2] * 16))
@@ -228,6 +284,47 @@ def big():
                         ti_hash=np.array(int((c0.right * np.arange(c0.right.size, dtype=np.int64)).sum())),
                         lvl_hash=np.array([int((c.row * 3 + c.col).sum()) for c in m.cores[1:]]))
     print("c4", coo.val.size, m.ranks[1])
+
+
+def round_fixtures():
+    """mpo_add (mpo.py:264-294), mpo_round (mpo.py:323-354) and the capped
+    matrix_to_mpo (sparse.py:260-275) run by the reference: output ranks
+    and the dense matrices (desk scale)."""
+    out = {}
+    # a redundant sum: exact rank 6 (5 + 1 shared directions) per bond,
+    # represented at rank 10 + noise at 1e-12 (kept at 1e-14, cut at 1e-10)
+    a = rmpo.random_mpo([2] * 7, [2] * 7, [5] * 6, seed=61)
+    b = rmpo.random_mpo([2] * 7, [2] * 7, [1] * 6, seed=62)
+    ab = rmpo.mpo_add(a, b)
+    noise = rmpo.random_mpo([2] * 7, [2] * 7, [2] * 6, seed=63)
+    noise = rmpo.Mpo([noise.cores[0] * 1e-12] + noise.cores[1:])
+    m = rmpo.mpo_add(rmpo.mpo_add(ab, a), noise)
+    pack_cores("add_a", a.cores, out)
+    pack_cores("add_b", b.cores, out)
+    pack_cores("add_ab", ab.cores, out)
+    pack_cores("round_in", m.cores, out)
+    for tag, tol in (("t10", 1e-10), ("t14", 1e-14), ("t6", 1e-6)):
+        r = rmpo.mpo_round(m, tol)
+        out[f"round_{tag}_ranks"] = np.array(r.ranks)
+        out[f"round_{tag}_dense"] = rmpo.contract_to_matrix(r)
+    out["round_in_dense"] = rmpo.contract_to_matrix(m)
+    # capped conversions
+    cases = [("rand64", rsparse.random_sparse_coo(64, 64, 0.2, seed=64), ([2] * 6, [2] * 6), 8, None),
+             ("band256", band_scatter(256, 600, seed=65), ([2] * 8, [2] * 8), 32, None),
+             ("rand64_t8", rsparse.random_sparse_coo(64, 64, 0.2, seed=66), ([2] * 6, [2] * 6), 8, 1e-8)]
+    for tag, coo, fac, cap, tol in cases:
+        plan = mposvd.plan_partition(coo.rows, coo.cols, fac)
+        mm = rsparse.matrix_to_mpo(coo, plan, rank_cap=cap, round_tol=tol)
+        out[f"cap_{tag}_rows"], out[f"cap_{tag}_cols"] = np.array(coo.rows), np.array(coo.cols)
+        out[f"cap_{tag}_row"], out[f"cap_{tag}_col"], out[f"cap_{tag}_val"] = coo.row, coo.col, coo.val
+        out[f"cap_{tag}_fac"] = np.array(fac)
+        out[f"cap_{tag}_cap"] = np.array(cap)
+        out[f"cap_{tag}_tol"] = np.array(np.nan if tol is None else tol)
+        out[f"cap_{tag}_ranks"] = np.array(mm.ranks)
+        out[f"cap_{tag}_dense"] = rmpo.contract_to_matrix(mm)
+        print(tag, mm.ranks)
+    np.savez_compressed(os.path.join(HERE, "round_add_cap.npz"), **out)
+    print("round fixtures written", {k: v for k, v in out.items() if k.endswith("_ranks")})
 
 
 def io_fixtures():
@@ -247,6 +344,8 @@ def io_fixtures():
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "--big":
         big()
+    elif len(sys.argv) > 1 and sys.argv[1] == "--round":
+        round_fixtures()
     elif len(sys.argv) > 1 and sys.argv[1] == "--io":
         io_fixtures()
     else:

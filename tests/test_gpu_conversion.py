@@ -152,3 +152,61 @@ def test_conversion_deterministic():
     a2 = m.convert_structure(r, c, v, plan).arrays()
     for x, y in zip(a1, a2):
         assert np.array_equal(x, y)
+
+
+def _sha(x):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+
+
+def test_conversion_c5_full_size_bit_exact():
+    """Config 5's conversion at its full size (2^22 square, 32.7M power-law
+    nonzeros): every index array bit-identical to the reference's
+    matrix_to_mpo run (sha256 digests in tests/golden/big_c5conv.npz,
+    sparse.py:207-258): i1, j1, ti, values and the level digits of three
+    cores."""
+    m = _api()
+    from paper_1707_07803_b200.workloads import powerlaw_coo, square_plan
+    z = load_golden("big_c5conv.npz")
+    r, c, v = powerlaw_coo(1 << 22, seed=55)
+    res = m.convert_structure(r, c, v, square_plan(22))
+    assert res.rank == int(z["rank"])
+    i1, j1, ti, vals, uniq = res.arrays()
+    assert ti.size == int(z["nnz"])
+    assert _sha(ti) == str(z["ti_sha"])
+    assert _sha(i1) == str(z["i1_sha"]) and _sha(j1) == str(z["j1_sha"])
+    assert _sha(vals) == str(z["values_sha"])
+    for k, lv in enumerate(z["levels"]):
+        rd, cd = res.level(int(lv))
+        assert _sha(rd) == str(z["lvl_row_sha"][k]) and _sha(cd) == str(z["lvl_col_sha"][k])
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_exchange_on_device(world):
+    """The multi-GPU conversion's per-rank kernels (local convert, sample
+    splitters, key-range merge, global-id search, remap) on one device, the
+    ranks run in lock step with their collectives emulated
+    (distributed.convert_sharded_emulated): config 5's recipe at 2^20,
+    bit-exact against the oracle's single-pass structure."""
+    import torch
+    from paper_1707_07803_b200.distributed import (DeviceOps, convert_sharded_emulated,
+                                                   shard_range)
+    from paper_1707_07803_b200.workloads import powerlaw_coo, square_plan
+    r, c, v = powerlaw_coo(1 << 20, seed=55)
+    v[::11] = 0.0   # explicit zeros are dropped before keying (sparse.py:234)
+    plan = square_plan(20)
+    ops = DeviceOps(0)
+    shards = []
+    for k in range(world):
+        lo, hi = shard_range(r.size, world, k)
+        shards.append(tuple(torch.from_numpy(x[lo:hi]).cuda() for x in (r, c, v)))
+    res = convert_sharded_emulated(shards, plan, ops)
+    st = orc.conversion_structure(r, c, v, plan.row_factors, plan.col_factors)
+    cat = lambda xs: np.concatenate([x.cpu().numpy() for x in xs])
+    assert np.array_equal(cat([x.ti for x in res]), st.ti)
+    assert np.array_equal(cat([x.i1 for x in res]), st.i1)
+    assert np.array_equal(cat([x.j1 for x in res]), st.j1)
+    assert np.array_equal(cat([x.values for x in res]), st.values)
+    assert np.array_equal(cat([x.uniq for x in res]), st.uniq)
+    assert all(x.rank == st.rank for x in res)
+    assert max(x.uniq.numel() for x in res) <= 1.25 * st.rank / world
