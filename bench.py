@@ -61,33 +61,69 @@ def ledger_flops(name):
 # CPU baseline samples (oracle = test infrastructure, only here and in tests)
 # ---------------------------------------------------------------------------
 
-def cpu_tnrsvd_sample(size=2048):
-    """The shapes that dominate config 2's ledger (the B-stage
-    truncation bonds): one dgesdd of a size x 2*size unfolding and one
-    dgeqrf+dorgqr of a 2*size x size unfolding, through the oracle's numpy
-    calls, rated with the same ledger formulas."""
+def blas_info():
+    """OpenBLAS/MKL build and thread count numpy uses on this host."""
+    try:
+        from threadpoolctl import threadpool_info
+        for x in threadpool_info():
+            if x.get("user_api") == "blas":
+                return {"library": f"{x.get('internal_api')} {x.get('version')}",
+                        "threads": int(x.get("num_threads") or 0)}
+    except Exception:  # pragma: no cover
+        pass
+    return {"library": "unknown", "threads": host_cores()}
+
+
+def cpu_c2_full(progress=None):
+    """The reference algorithm end to end on config 2 (the oracle
+    restatement of rsvd.py:217-259, same numpy/LAPACK calls, OpenBLAS on all
+    host cores): one complete tnrsvd, its ledger flops counted live.
+    ``progress(ledger_total)`` is called after every LAPACK/BLAS call."""
     from oracle import mposvd_oracle as orc
-    rng = np.random.default_rng(0)
-    m_svd = rng.standard_normal((size, 2 * size))
-    m_qr = rng.standard_normal((2 * size, size))
+    from paper_1707_07803_b200.workloads import TNRSVD_ARGS, config_mpo
+    kw = dict(TNRSVD_ARGS["c2"])
+    a = [np.ascontiguousarray(c) for c in config_mpo("c2").cores]
+    led = orc.Ledger()
+    if progress is not None:
+        add = led.add
+
+        def hooked(kind, flops, shape):
+            add(kind, flops, shape)
+            progress(led.total)
+        led.add = hooked
     t0 = time.perf_counter()
-    np.linalg.svd(m_svd, full_matrices=False)
-    np.linalg.qr(m_qr)
+    res = orc.tnrsvd(a, kw.pop("k_target"), ledger=led, **kw)
     secs = time.perf_counter() - t0
-    flops = orc._svd_flops(size, 2 * size) + orc._qr_flops(2 * size, size)
-    return flops / secs / 1e12, secs, (f"c2 B-stage bond shapes: dgesdd {size}x{2 * size} + "
-                                      f"dgeqrf/dorgqr {2 * size}x{size} (numpy/OpenBLAS)")
+    return led.total, secs, res
 
 
-def cpu_conversion_sample(log2n=18):
+def cpu_c1_median():
+    """Config 1 through the oracle, median of 3 (reference bench.py:148-155)."""
+    from oracle import mposvd_oracle as orc
+    from paper_1707_07803_b200.workloads import TNRSVD_ARGS, config_mpo
+    kw = dict(TNRSVD_ARGS["c1"])
+    a = [np.ascontiguousarray(c) for c in config_mpo("c1").cores]
+    k = kw.pop("k_target")
+    _, secs = orc.timed(lambda: orc.tnrsvd([c.copy() for c in a], k, **kw), repeats=3)
+    return secs
+
+
+def cpu_conversion_full(log2n=22):
+    """Config 5's whole conversion through the oracle port of matrix_to_mpo
+    (sparse.py:207-258 with SparseCore index arrays, single-threaded numpy,
+    as the reference) and, separately, the SparseMatrixCoo constructor's
+    validation (sparse.py:53-70)."""
     from oracle import mposvd_oracle as orc
     from paper_1707_07803_b200.workloads import powerlaw_coo
-    r, c, v = powerlaw_coo(1 << log2n, seed=55)
-    rf = cf = (2,) * log2n
+    n = 1 << log2n
+    r, c, v = powerlaw_coo(n, seed=55)
     t0 = time.perf_counter()
-    orc.conversion_structure(r, c, v, rf, cf)
-    secs = time.perf_counter() - t0
-    return r.size / secs, secs, f"config-5 recipe at 2^{log2n} ({r.size} nnz), oracle sparse.py:234-250"
+    orc.coo_validate(n, n, r, c, v)
+    t_ctor = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orc.matrix_to_mpo_arrays(r, c, v, (2,) * log2n, (2,) * log2n)
+    t_conv = time.perf_counter() - t0
+    return r.size, t_conv, t_ctor
 
 
 def host_cores():
@@ -175,27 +211,50 @@ class Clocks:
 # ---------------------------------------------------------------------------
 
 def run_reference(args, rank, world):
+    """The reference's CPU implementation of the headline path on this
+    box's host cores: config 2's tnrsvd end to end (the oracle restatement,
+    same numpy/OpenBLAS calls; /root/reference does not travel to the GPU
+    box).  Warm-up: W config-1 runs.  Timed region: ONE complete config-2
+    run (~2 min) -- the --steps K are K equal slices of its flop ledger, so
+    ms_per_step = total / K and value = ledger flops / total time."""
     if rank != 0:
         return
-    for _ in range(args.warmup):
-        cpu_tnrsvd_sample()
-    vals = []
+    from oracle import mposvd_oracle as orc
+    from paper_1707_07803_b200.workloads import TNRSVD_ARGS, config_mpo
+    kw1 = dict(TNRSVD_ARGS["c1"])
+    a1 = [np.ascontiguousarray(c) for c in config_mpo("c1").cores]
+    k1 = kw1.pop("k_target")
+    for _ in range(max(args.warmup, 0)):
+        orc.tnrsvd([c.copy() for c in a1], k1, **kw1)
+    total = ledger_flops("c2")
+    marks = []
+    steps = max(args.steps, 1)
+
+    def progress(done):
+        while len(marks) < steps and done >= total * (len(marks) + 1) / steps * (1 - 1e-12):
+            marks.append(time.perf_counter())
+
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, secs, sample = cpu_tnrsvd_sample()
-        vals.append(v)
-    wall = time.perf_counter() - t0
-    value = statistics.median(vals)
+    flops, secs, res = cpu_c2_full(progress)
+    step_s = [b - a for a, b in zip([t0] + marks[:-1], marks)] if len(marks) == steps else []
+    value = flops / secs / 1e12
+    blas = blas_info()
+    sample = (f"one complete config-2 tnrsvd (oracle port of rsvd.py:217-259, numpy "
+              f"{np.__version__}, {blas['library']}, {blas['threads']} threads), timed as "
+              f"{steps} equal-ledger steps; ledger {flops:.4g} flops")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+        "n_gpus": world, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "c2 TNrSVD (BASELINE configs[1]); CPU sample of its dominant "
-                               "bond factorizations"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": host_cores(), "kind": "port",
-                         "sample": sample},
+        "config": {"workload": "c2: TNrSVD of random MPO d=20 n=2 rank 8 (N(0,1)/sqrt(8)), "
+                               "K=20 p=10 q=1 round_tol=1e-9",
+                   "time_to_k_triplets_s": secs},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": blas["threads"], "kind": "port",
+                         "sample": sample, "seconds": secs},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_seconds": step_s,
+        "s_head": [float(x) for x in res.s[:3]],
     }
     print(json.dumps(line), flush=True)
 
@@ -373,6 +432,7 @@ def run_b200(args, rank, world, local_rank):
     if not args.no_conversion:
         line["conversion"] = bench_conversion(args, torch, dist, rank, world, dev, barrier,
                                               max_over_ranks)
+    line["c1"] = bench_c1(args, torch, rank, world, barrier, max_over_ranks)
     if not args.no_c3:
         line["tnrsvd_c3q0"] = bench_c3q0(args, torch, rank, world, barrier, max_over_ranks)
     if not args.no_batched:
@@ -381,16 +441,66 @@ def run_b200(args, rank, world, local_rank):
         line["tnrsvd_batched_q0"] = bench_batched(args, torch, rank, world, barrier,
                                                   max_over_ranks, cfg="c5inst_q0")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, secs, sample = cpu_tnrsvd_sample()
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "port",
-                                "sample": sample, "seconds": secs}
+        fl, secs, _ = cpu_c2_full()
+        blas = blas_info()
+        line["cpu_baseline"] = {
+            "value": fl / secs / 1e12, "unit": UNIT, "cores": blas["threads"], "kind": "port",
+            "sample": f"one complete config-2 tnrsvd, oracle port of rsvd.py:217-259 (numpy "
+                      f"{np.__version__}, {blas['library']}); {secs:.1f} s to K triplets vs "
+                      f"{per_step:.3f} s on the B200", "seconds": secs}
+        if "c1" in line:
+            cs1 = cpu_c1_median()
+            line["c1"]["cpu_baseline"] = {"value": cs1 * 1e3, "unit": "ms", "cores": blas["threads"],
+                                          "kind": "port", "sample": "config-1 tnrsvd, oracle, "
+                                          "median of 3 (reference bench.py:148-155)"}
         if "conversion" in line:
-            cv, cs, csample = cpu_conversion_sample()
-            line["conversion"]["cpu_baseline"] = {"value": cv, "unit": "nnz/s", "cores": 1,
-                                                  "kind": "port", "sample": csample,
-                                                  "seconds": cs}
+            nnz, tc, tctor = cpu_conversion_full()
+            line["conversion"]["cpu_baseline"] = {
+                "value": nnz / tc, "unit": "nnz/s", "cores": 1, "kind": "port",
+                "sample": "config 5 at 2^22 (32.7M nnz): oracle port of the whole uncapped "
+                          "matrix_to_mpo (sparse.py:207-258, SparseCore index arrays), "
+                          "single-threaded numpy as the reference",
+                "seconds": tc, "coo_constructor_seconds": tctor}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def bench_c1(args, torch, rank, world, barrier, max_over_ranks, steps=20):
+    """Config 1 (BASELINE configs[0]: d=10 n=2 rank 3, K=10, p=10, q=0) --
+    the latency-bound regime: device time per tnrsvd on resident inputs and
+    end to end through tnrsvd(host Mpo) (upload + download inside)."""
+    import paper_1707_07803_b200 as m
+    from paper_1707_07803_b200.rsvd import prepare, tnrsvd_prepared
+    from paper_1707_07803_b200.workloads import TNRSVD_ARGS, config_mpo
+    kw = TNRSVD_ARGS["c1"]
+    a = config_mpo("c1")
+    am, o, _ = prepare(a, kw["k_target"], kw["oversample"], kw["seed"])
+    for _ in range(3):
+        tnrsvd_prepared(am, o, kw["k_target"], kw["q"], kw["round_tol"])
+        m.tnrsvd(a, **kw)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        tnrsvd_prepared(am, o, kw["k_target"], kw["q"], kw["round_tol"])
+    e1.record()
+    e1.synchronize()
+    dev_ms = max_over_ranks(e0.elapsed_time(e1) / steps)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        lr = m.tnrsvd(a, **kw)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / steps)
+    return {"metric": "config-1 TNrSVD time-to-K-triplets", "value": dev_ms, "unit": "ms",
+            "higher_is_better": False, "n_gpus": world, "scaling": "weak",
+            "e2e": {"value": e2e_ms, "unit": "ms",
+                    "h2d_bytes_per_step": int(sum(c.nbytes for c in a.cores)),
+                    "d2h_bytes_per_step": int(sum(c.nbytes for c in lr.u.cores) +
+                                              sum(c.nbytes for c in lr.v.cores) + lr.s.nbytes),
+                    "api": "paper_1707_07803_b200.tnrsvd(host Mpo)"},
+            "s_head": [float(x) for x in lr.s[:3]]}
 
 
 def bench_c3q0(args, torch, rank, world, barrier, max_over_ranks):
@@ -490,7 +600,11 @@ def bench_batched(args, torch, rank, world, barrier, max_over_ranks, n_inst=64, 
 
 def bench_conversion(args, torch, dist, rank, world, dev, barrier, max_over_ranks):
     """Config 5's conversion: 2^22 square, power-law rows (alpha 2.1), uniform
-    columns, U(-1,1) values, plan ([2]*22, [2]*22); nnz sharded over ranks."""
+    columns, U(-1,1) values, plan ([2]*22, [2]*22); nnz sharded over ranks
+    (contiguous input ranges), block keys exchanged by key range
+    (distributed.py: samples -> splitters, one all-to-all of keys, one back
+    of global ids).  The timed region covers the whole sharded conversion
+    incl. the exchange; the input (785 MB of COO) exceeds the 126 MB L2."""
     from paper_1707_07803_b200.distributed import DeviceOps, convert_sharded, shard_range
     from paper_1707_07803_b200.workloads import powerlaw_coo, square_plan
     r, c, v = powerlaw_coo(1 << 22, seed=55)
@@ -518,49 +632,78 @@ def bench_conversion(args, torch, dist, rank, world, dev, barrier, max_over_rank
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6521.1
     achieved = compulsory / secs / 1e9 / world   # per GPU
     try:
-        ctraffic = json.load(open(os.path.join(ROOT, "profiles", "r01_conv_traffic.json")))
+        ctraffic = json.load(open(os.path.join(ROOT, "profiles", "conv_traffic.json")))
     except (OSError, ValueError):
         ctraffic = {}
-    # end to end: host COO in, host (i1, j1, ti, values, uniq) out
-    import paper_1707_07803_b200 as m
-    rs, cs_, vs = r[lo:hi], c[lo:hi], v[lo:hi]
-    for _ in range(args.warmup):   # populates the pinned host pool of the downloads
-        rr = m.convert_structure(rs, cs_, vs, plan)
-        arrs = rr.arrays()
-        rr.free()
-    del arrs
+    # end to end through the sharded path: this rank's host COO shard
+    # (pinned) -> HBM, conversion + exchange, (i1, j1, ti, values, uniq
+    # shard) -> pinned host
+    pin = lambda x: torch.from_numpy(x).pin_memory()
+    hr, hc, hv = pin(r[lo:hi]), pin(c[lo:hi]), pin(v[lo:hi])
+    outs = None
+
+    def e2e_step():
+        nonlocal outs
+        res = convert_sharded(hr.to(dev, non_blocking=True), hc.to(dev, non_blocking=True),
+                              hv.to(dev, non_blocking=True), plan, ops)
+        arrs = (res.i1, res.j1, res.ti, res.values, res.uniq)
+        if outs is None or any(o.numel() != a.numel() for o, a in zip(outs, arrs)):
+            outs = [torch.empty(a.numel(), dtype=a.dtype, pin_memory=True) for a in arrs]
+        for o, a in zip(outs, arrs):
+            o.copy_(a, non_blocking=True)
+        torch.cuda.synchronize()
+        return sum(o.numel() * o.element_size() for o in outs)
+
+    for _ in range(args.warmup):
+        d2h = e2e_step()
+    barrier()
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        rr = m.convert_structure(rs, cs_, vs, plan)
-        arrs = rr.arrays()
-        rr.free()
+        d2h = e2e_step()
     e2e = max_over_ranks((time.perf_counter() - t0) / args.steps)
     return {
         "metric": "sparse->MPO conversion nnz/s (config 5, 2^22 power-law, d=22)",
         "value": n / secs, "unit": "nnz/s", "n_gpus": world, "scaling": "strong",
         "nnz": int(n), "blocks": int(blocks), "ms_per_step": secs * 1e3,
+        "input_order": "row-sorted COO (deduplicated by np.unique)",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                      "frac": achieved / peak_hbm,
                      "traffic": ctraffic.get("dram_bytes_per_step"),
                      "traffic_source": ctraffic.get("source"),
                      "algorithmic_bytes_per_step": compulsory,
-                     "note": "whole conversion (compaction + onesweep radix passes + segment) timed; "
-                             "compulsory bytes 32 B/nnz + 8 B/block"},
-        "e2e": {"value": (hi - lo) * world / e2e if world > 1 else n / e2e, "unit": "nnz/s",
-                "h2d_bytes_per_step": int(24 * (hi - lo)),
-                "d2h_bytes_per_step": int(sum(a.nbytes for a in arrs)),
-                "api": "convert_structure(host COO) + arrays() (single-rank shard path)"},
+                     "note": "whole conversion (compaction + radix passes + segment + ids) "
+                             "timed; compulsory bytes 32 B/nnz + 8 B/block (SURVEY 8(d))"},
+        "e2e": {"value": n / e2e, "unit": "nnz/s",
+                "h2d_bytes_per_step": int(24 * (hi - lo)) * world,
+                "d2h_bytes_per_step": int(d2h) * world,
+                "api": "distributed.convert_sharded on each rank's pinned host shard "
+                       "(H2D, convert + key-range exchange, D2H of i1/j1/ti/values/uniq)"},
     }
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torchrun (rank 0 prints the line)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if world != args.gpus and rank == 0:
+        print(f"[bench] note: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}",
+              file=sys.stderr)
     if world > 1:
         import torch
         import torch.distributed as dist
