@@ -97,6 +97,10 @@ int mpo_add(mpo_ctx* ctx, const mpo_dev* a, const mpo_dev* b, mpo_dev** out);
 /* ---- sparse -> MPO conversion (sparse.py:207-258, uncapped path) ------- */
 /* row1/col1: 1-based int64 coordinates, val: FP64, n entries (explicit zeros
  * are dropped, sparse.py:234); factors: the PartitionPlan (partition.py:40). */
+/* from_host = 0: row1/col1/val are device arrays that must stay valid until
+ * mpo_conv_free (without explicit zeros the entry arrays i1, j1, values are
+ * derived from them on demand); from_host = 1: host arrays, uploaded and
+ * kept by the handle. */
 int mpo_sparse_convert(mpo_ctx* ctx, const int64_t* row1, const int64_t* col1,
                        const double* val, int64_t n, int from_host, int d,
                        const int64_t* row_factors, const int64_t* col_factors, mpo_conv** out);
@@ -104,6 +108,11 @@ int mpo_conv_info(const mpo_conv* c, int64_t* nkept, int64_t* rank);
 /* any output pointer may be NULL; sizes nkept (i1, j1, ti, values) and rank (uniq) */
 int mpo_conv_copy(mpo_ctx* ctx, const mpo_conv* c, int64_t* i1, int64_t* j1, int64_t* ti,
                   double* values, int64_t* uniq, int to_host);
+/* device pointers of the handle's arrays (owned by the handle, valid until
+ * mpo_conv_free; any output may be NULL).  Requesting i1, j1 or values
+ * materialises them if they were left derivable (no explicit zeros). */
+int mpo_conv_ptrs(mpo_ctx* ctx, const mpo_conv* c, int64_t** i1, int64_t** j1, int64_t** ti,
+                  double** values, int64_t** uniq);
 /* block digits of core `level` (1..d-1), level-2 fastest (sparse.py:173-180, :249-250) */
 int mpo_conv_level(mpo_ctx* ctx, const mpo_conv* c, int level, int64_t* row_digits,
                    int64_t* col_digits, int to_host);

@@ -55,6 +55,8 @@ SIGNATURES = {
                                      _I64P, C.POINTER(_P)]),
     "mpo_conv_info": (C.c_int, [_P, _I64P, _I64P]),
     "mpo_conv_copy": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, C.c_int]),
+    "mpo_conv_ptrs": (C.c_int, [_P, _P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
+                                C.POINTER(_P), C.POINTER(_P)]),
     "mpo_conv_level": (C.c_int, [_P, _P, C.c_int, _P, _P, C.c_int]),
     "mpo_conv_dense_core": (C.c_int, [_P, _P, C.c_int, _P, C.c_int]),
     "mpo_conv_chunk": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.POINTER(_P)]),

@@ -298,6 +298,10 @@ MPO_API int mpo_sparse_convert(mpo_ctx* ctx, const int64_t* row1, const int64_t*
         r = hr.get(); cc = hc.get(); v = hv.get();
       }
       c->c = mpob::convert_local(st, r, cc, v, n, rf[0], cf[0], c->nrb, ncb);
+      // lazily derived entries read the uploads: the handle keeps them
+      c->c.own_row = std::move(hr);
+      c->c.own_col = std::move(hc);
+      c->c.own_val = std::move(hv);
     } catch (...) {
       delete c;
       throw;
@@ -317,6 +321,7 @@ MPO_API int mpo_conv_copy(mpo_ctx* ctx, const mpo_conv* c, int64_t* i1, int64_t*
   return guarded(ctx, [&] {
     const cudaStream_t st = ctx->stream;
     const int64_t n = c->c.nkept, r = c->c.rank;
+    if (i1 || j1 || values) mpob::ensure_entries(st, const_cast<mpo_conv*>(c)->c);
     auto cp = [&](void* dst, const void* src, size_t bytes) {
       if (dst && bytes) CK(cudaMemcpyAsync(dst, src, bytes, kind_out(to_host), st));
     };
@@ -326,6 +331,19 @@ MPO_API int mpo_conv_copy(mpo_ctx* ctx, const mpo_conv* c, int64_t* i1, int64_t*
     cp(values, c->c.values.get(), sizeof(double) * n);
     cp(uniq, c->c.uniq.get(), sizeof(int64_t) * r);
     if (to_host) CK(cudaStreamSynchronize(st));
+  });
+}
+
+MPO_API int mpo_conv_ptrs(mpo_ctx* ctx, const mpo_conv* c, int64_t** i1, int64_t** j1,
+                          int64_t** ti, double** values, int64_t** uniq) {
+  return guarded(ctx, [&] {
+    auto& cl = const_cast<mpo_conv*>(c)->c;
+    if (i1 || j1 || values) mpob::ensure_entries(ctx->stream, cl);
+    if (i1) *i1 = cl.i1.get();
+    if (j1) *j1 = cl.j1.get();
+    if (ti) *ti = cl.ti.get();
+    if (values) *values = cl.values.get();
+    if (uniq) *uniq = cl.uniq.get();
   });
 }
 
@@ -355,6 +373,7 @@ MPO_API int mpo_conv_chunk(mpo_ctx* ctx, const mpo_conv* c, int64_t start, int64
     need(start >= 0 && stop > start && stop <= c->c.rank, "chunk out of range");
     const int d = (int)c->rf.size();
     const int64_t sub = stop - start;
+    mpob::ensure_entries(ctx->stream, const_cast<mpo_conv*>(c)->c);
     mpob::Cores cs;
     for (int k = 0; k < d; ++k) {
       mpob::Core core = k == 0 ? mpob::make_core(ctx->stream, 1, c->rf[0], c->cf[0], sub)
@@ -374,6 +393,7 @@ MPO_API int mpo_conv_dense_core(mpo_ctx* ctx, const mpo_conv* c, int level, doub
     need(level >= 0 && level < d, "level out of range");
     need(c->c.rank >= 1, "no blocks");
     const cudaStream_t st = ctx->stream;
+    if (level == 0) mpob::ensure_entries(st, const_cast<mpo_conv*>(c)->c);
     const int64_t r = c->c.rank;
     int64_t sz = (level == 0) ? c->rf[0] * c->cf[0] * r
                               : r * c->rf[level] * c->cf[level] * (level == d - 1 ? 1 : r);

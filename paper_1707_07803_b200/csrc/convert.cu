@@ -485,6 +485,7 @@ ConvLocal convert_local(cudaStream_t st, const int64_t* row1, const int64_t* col
                         int64_t ncb) {
   ConvLocal c;
   if (n < 0) throw ValueError("negative nonzero count");
+  if (convert_fast(st, row1, col1, val, n, I1, J1, nrb, ncb, c)) return c;
   const int64_t tiles = grid_tiles(n);
   DBuf<unsigned> cnt(tiles, st);
   DBuf<int64_t> toff(tiles, st), tot(1, st);

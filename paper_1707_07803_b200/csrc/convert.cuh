@@ -15,7 +15,23 @@ struct ConvLocal {
   DBuf<double> values;
   int64_t nkept = 0;
   int64_t rank = 0;
+  // lazy entries (fast path, no explicit zeros): i1, j1, values are derived
+  // from the input on demand (ensure_entries); the input must outlive it --
+  // host uploads are owned here, device inputs are the caller's
+  bool lazy = false;
+  const int64_t* src_row = nullptr;
+  const int64_t* src_col = nullptr;
+  const double* src_val = nullptr;
+  int64_t I1 = 1, J1 = 1;
+  DBuf<int64_t> own_row, own_col;
+  DBuf<double> own_val;
 };
+
+// bucketed fast path (convert_fast.cu); false: not applicable (the caller
+// takes the onesweep path), c untouched
+bool convert_fast(cudaStream_t st, const int64_t* row1, const int64_t* col1, const double* val,
+                  int64_t n, int64_t I1, int64_t J1, int64_t nrb, int64_t ncb, ConvLocal& c);
+void ensure_entries(cudaStream_t st, ConvLocal& c);
 
 ConvLocal convert_local(cudaStream_t st, const int64_t* row1, const int64_t* col1,
                         const double* val, int64_t n, int64_t I1, int64_t J1, int64_t nrb,

@@ -1,0 +1,586 @@
+// Sparse -> MPO conversion structure, bucketed fast path (sm_100a).
+//
+// Same result as the onesweep pipeline in convert.cu -- np.unique(key,
+// return_inverse=True) of the kept block keys, sparse.py:234-250 -- with
+// about half the DRAM traffic, by sorting MSD-first into buckets that fit one
+// CTA's shared memory and finishing each bucket on chip:
+//
+//   K1 fast_hist     per 16K-entry tile: histogram of the bucket (key >> s)
+//                    of every kept entry, kept count          read col (+row), val
+//   K2 fast_scan_*   per-bucket tile offsets, bucket starts, kept offsets
+//   K3 fast_scatter  per tile: key, bucket, 64-bit item (low key | position),
+//                    staged by bucket in shared memory, written as runs into
+//                    the bucket regions                        read row, col, val;
+//                                                              write 8 B / entry
+//   K4 fast_bucket   per bucket (<= 16K entries, taken in bucket order from a
+//                    ticket): stable LSD sort of the low key bits on chip
+//                    (10-bit digits, warp-private counters + __match_any),
+//                    head flags -> local block ids, decoupled look-back over
+//                    the preceding buckets for the global id offset, then
+//                    uniq (coalesced) and ti[position]        read 8 B, write
+//                                                              8 B/block + 8 B
+// Compulsory traffic is 32 B/entry + 8 B/block; this path
+// moves ~64 B/entry + 8 B/block plus the random ti scatter.  Ties between
+// equal keys are never ordered by anything observable (ids only), so the
+// in-tile slot order (shared-memory atomics) does not affect the output,
+// which is bit-identical to the reference's.
+//
+// Without explicit zeros the per-entry (i1, j1, values) arrays are not
+// written here at all: they are derivable from the input (i1 = (row-1) % I1,
+// values = val) and are materialised on demand (ensure_entries).
+#include "common.cuh"
+#include "convert.cuh"
+#include "kernels.cuh"
+
+namespace mpob {
+
+namespace {
+
+constexpr int F_CT = 512;                 // tile CTAs (K1, K3)
+constexpr int F_IT = 32;
+constexpr int F_TILE = F_CT * F_IT;       // 16384 entries per tile
+constexpr int F_MAXB = 4096;              // buckets
+constexpr int B_CT = 512;                 // bucket CTAs (K4)
+constexpr int B_W = B_CT / 32;
+constexpr int B_IT = 32;
+constexpr int B_CAP = B_CT * B_IT;        // 16384 entries per bucket
+constexpr int B_RB = 10;
+constexpr int B_R = 1 << B_RB;            // local digit bins
+constexpr unsigned long long ST_AGG = 1ull << 62, ST_PRE = 2ull << 62,
+                             ST_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct KeyMap {
+  int64_t I1, J1, nrb;
+  int s;          // bucket = key >> s
+  int bc_shift;   // >= 0: bucket = bc >> bc_shift (no row needed); -1: full key
+};
+
+__device__ __forceinline__ uint64_t entry_key(const KeyMap& m, int64_t r1, int64_t c1) {
+  const int64_t br = (r1 - 1) / m.I1, bc = (c1 - 1) / m.J1;
+  return (uint64_t)(br + m.nrb * bc);
+}
+
+// ---------------- K1 -------------------------------------------------------
+__global__ void __launch_bounds__(F_CT) fast_hist(const int64_t* __restrict__ row1,
+                                                  const int64_t* __restrict__ col1,
+                                                  const double* __restrict__ val, int64_t n,
+                                                  KeyMap m, int nb, unsigned* __restrict__ thist,
+                                                  unsigned* __restrict__ tkept) {
+  __shared__ unsigned h[F_MAXB];
+  __shared__ unsigned wsum[F_CT / 32];
+  for (int i = threadIdx.x; i < nb; i += F_CT) h[i] = 0;
+  __syncthreads();
+  const int64_t base = blockIdx.x * (int64_t)F_TILE;
+  unsigned c = 0;
+  constexpr int U = 8;   // loads in flight per thread
+#pragma unroll 1
+  for (int it0 = 0; it0 < F_IT; it0 += U) {
+    int64_t cv[U];
+    double vv[U];
+    int64_t rv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (it0 + u) * F_CT + threadIdx.x;
+      const bool ok = i < n;
+      cv[u] = ok ? col1[i] : 1;
+      vv[u] = ok ? val[i] : 0.0;
+      rv[u] = (ok && m.bc_shift < 0) ? row1[i] : 1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (vv[u] != 0.0) {
+        unsigned b;
+        if (m.bc_shift >= 0) b = (unsigned)(((cv[u] - 1) / m.J1) >> m.bc_shift);
+        else b = (unsigned)(entry_key(m, rv[u], cv[u]) >> m.s);
+        atomicAdd(&h[b], 1u);
+        ++c;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < F_CT / 32; ++w) t += wsum[w];
+    tkept[blockIdx.x] = t;
+  }
+  unsigned* out = thist + (int64_t)blockIdx.x * nb;
+  for (int i = threadIdx.x; i < nb; i += F_CT) out[i] = h[i];
+}
+
+// ---------------- K2 -------------------------------------------------------
+// per bucket (lane), 8 warps over contiguous tile segments: tile prefix of
+// the bucket counts (toff, without the bucket start) and the bucket totals
+__global__ void __launch_bounds__(256) fast_scan_tiles(const unsigned* __restrict__ thist,
+                                                       int ntiles, int nb,
+                                                       unsigned* __restrict__ toff,
+                                                       unsigned* __restrict__ tot) {
+  __shared__ unsigned ssum[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.x * 32 + lane;
+  const int seg = (ntiles + 7) / 8;
+  const int t0 = warp * seg, t1 = min(ntiles, t0 + seg);
+  unsigned s = 0;
+  if (b < nb)
+    for (int t = t0; t < t1; ++t) s += thist[(int64_t)t * nb + b];
+  ssum[warp][lane] = s;
+  __syncthreads();
+  unsigned run = 0;
+  for (int w = 0; w < warp; ++w) run += ssum[w][lane];
+  if (b < nb) {
+    for (int t = t0; t < t1; ++t) {
+      const int64_t o = (int64_t)t * nb + b;
+      const unsigned v = thist[o];
+      toff[o] = run;
+      run += v;
+    }
+    if (warp == 7) tot[b] = run;
+  }
+}
+
+// bucket starts (exclusive scan of the totals), the largest bucket, kept
+// offsets per tile and the kept total: one CTA
+__global__ void __launch_bounds__(1024) fast_scan_buckets(const unsigned* __restrict__ tot, int nb,
+                                                          const unsigned* __restrict__ tkept,
+                                                          int ntiles,
+                                                          int64_t* __restrict__ bstart,
+                                                          int64_t* __restrict__ tkoff,
+                                                          int64_t* __restrict__ info) {
+  __shared__ int64_t sh[1024];
+  __shared__ unsigned smax[32];
+  auto scan = [&](auto get, auto put, int count, int64_t* total) {
+    int64_t carry = 0;
+    for (int base = 0; base < count; base += 1024) {
+      const int i = base + threadIdx.x;
+      const int64_t v = i < count ? get(i) : 0;
+      sh[threadIdx.x] = v;
+      __syncthreads();
+      for (int o = 1; o < 1024; o <<= 1) {
+        const int64_t add = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+        __syncthreads();
+        sh[threadIdx.x] += add;
+        __syncthreads();
+      }
+      if (i < count) put(i, carry + sh[threadIdx.x] - v);
+      carry += sh[1023];
+      __syncthreads();
+    }
+    if (total) *total = carry;
+  };
+  unsigned mx = 0;
+  for (int i = threadIdx.x; i < nb; i += 1024) mx = max(mx, tot[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = mx;
+  int64_t nk = 0;
+  scan([&](int i) { return (int64_t)tot[i]; }, [&](int i, int64_t v) { bstart[i] = v; }, nb, nullptr);
+  scan([&](int i) { return (int64_t)tkept[i]; }, [&](int i, int64_t v) { tkoff[i] = v; }, ntiles,
+       &nk);
+  if (threadIdx.x == 0) {
+    unsigned m = 0;
+    for (int w = 0; w < 32; ++w) m = max(m, smax[w]);
+    info[0] = nk;
+    info[1] = m;
+  }
+}
+
+// ---------------- K3 -------------------------------------------------------
+struct ScatterArgs {
+  const int64_t* row1;
+  const int64_t* col1;
+  const double* val;
+  int64_t n;
+  KeyMap m;
+  int nb, pbits;
+  const unsigned* thist;
+  const unsigned* toff;
+  const int64_t* bstart;
+  const int64_t* tkoff;
+  bool zeros;          // explicit zeros present: compact, write i1/j1/values
+  uint64_t* items;
+  int64_t* i1;
+  int64_t* j1;
+  double* values;
+};
+
+constexpr size_t K3_SMEM = (size_t)F_TILE * (sizeof(uint64_t) + sizeof(uint16_t)) +
+                           2 * (size_t)F_MAXB * sizeof(unsigned);
+
+__global__ void __launch_bounds__(F_CT) fast_scatter(ScatterArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  uint64_t* sitem = reinterpret_cast<uint64_t*>(sm);
+  unsigned* loff = reinterpret_cast<unsigned*>(sm + (size_t)F_TILE * sizeof(uint64_t));
+  unsigned* cur = loff + F_MAXB;
+  uint16_t* sb = reinterpret_cast<uint16_t*>(cur + F_MAXB);
+  __shared__ unsigned wpart[F_CT / 32];
+  __shared__ unsigned s_total;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = a.nb;
+  const unsigned* hrow = a.thist + (int64_t)blockIdx.x * nb;
+  // tile-local bucket offsets: exclusive scan of this tile's histogram row
+  {
+    constexpr int PER = F_MAXB / F_CT;   // 8 buckets per thread (nb <= 4096)
+    unsigned v[PER], s = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int b = tid * PER + q;
+      v[q] = b < nb ? hrow[b] : 0u;
+      s += v[q];
+    }
+    unsigned inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wpart[warp] = inc;
+    __syncthreads();
+    unsigned wb = 0, tt = 0;
+    for (int w = 0; w < F_CT / 32; ++w) { const unsigned x = wpart[w]; wb += w < warp ? x : 0; tt += x; }
+    unsigned run = wb + inc - s;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int b = tid * PER + q;
+      if (b < nb) { loff[b] = run; cur[b] = 0; }
+      run += v[q];
+    }
+    if (tid == 0) s_total = tt;
+  }
+  __syncthreads();
+  const int64_t base = blockIdx.x * (int64_t)F_TILE;
+  int64_t kbase = a.zeros ? a.tkoff[blockIdx.x] : base;
+  const uint64_t lowmask = a.m.s >= 64 ? ~0ull : ((1ull << a.m.s) - 1);
+#pragma unroll 1
+  for (int it = 0; it < F_IT; ++it) {
+    const int64_t i = base + it * F_CT + tid;
+    const bool ok = i < a.n;
+    const int64_t r1 = ok ? a.row1[i] : 1, c1 = ok ? a.col1[i] : 1;
+    const double v = ok ? a.val[i] : 0.0;
+    const bool keep = ok && v != 0.0;
+    int64_t pos;
+    if (a.zeros) {
+      // kept index in input order: ballot + warp prefix for this round
+      const unsigned ball = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) wpart[warp] = __popc(ball);
+      __syncthreads();
+      unsigned before = 0, tot = 0;
+      for (int w = 0; w < F_CT / 32; ++w) { const unsigned x = wpart[w]; before += w < warp ? x : 0; tot += x; }
+      pos = kbase + before + __popc(ball & lanemask_lt());
+      kbase += tot;
+      __syncthreads();
+    } else {
+      pos = i;
+    }
+    if (keep) {
+      const int64_t r0 = r1 - 1, c0 = c1 - 1;
+      const int64_t br = r0 / a.m.I1, bc = c0 / a.m.J1;
+      const uint64_t key = (uint64_t)(br + a.m.nrb * bc);
+      const unsigned b = (unsigned)(key >> a.m.s);
+      const unsigned slot = atomicAdd(&cur[b], 1u);   // in-tile slot: order irrelevant
+      const unsigned j = loff[b] + slot;
+      sitem[j] = ((key & lowmask) << a.pbits) | (uint64_t)pos;
+      sb[j] = (uint16_t)b;
+      if (a.zeros) {
+        a.i1[pos] = r0 - br * a.m.I1;
+        a.j1[pos] = c0 - bc * a.m.J1;
+        a.values[pos] = v;
+      }
+    }
+  }
+  __syncthreads();
+  // global start of this tile's run in each bucket (n < 2^31: fits 32 bits)
+  const unsigned* trow = a.toff + (int64_t)blockIdx.x * nb;
+  for (int b = tid; b < nb; b += F_CT) cur[b] = (unsigned)(a.bstart[b] + trow[b]) - loff[b];
+  __syncthreads();
+  const unsigned cnt = s_total;
+  for (unsigned j = tid; j < cnt; j += F_CT) a.items[cur[sb[j]] + j] = sitem[j];
+}
+
+// ---------------- K4 -------------------------------------------------------
+struct BucketArgs {
+  const uint64_t* items;
+  const unsigned* tot;
+  const int64_t* bstart;
+  int nb, s, pbits;
+  unsigned* ticket;
+  unsigned long long* status;
+  int64_t* uniq;
+  int64_t* ti;
+  int64_t* rank_out;
+};
+
+constexpr size_t K4_SMEM = (size_t)B_CAP * sizeof(uint64_t) +
+                           (size_t)B_W * B_R * sizeof(uint16_t) + (size_t)B_R * sizeof(unsigned);
+
+__global__ void __launch_bounds__(B_CT, 1) fast_bucket(BucketArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  uint64_t* A = reinterpret_cast<uint64_t*>(sm);
+  uint16_t* wh = reinterpret_cast<uint16_t*>(sm + (size_t)B_CAP * sizeof(uint64_t));
+  unsigned* dst0 = reinterpret_cast<unsigned*>(wh + B_W * B_R);
+  __shared__ unsigned s_b, wtot[B_W];
+  __shared__ int64_t s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_b = atomicAdd(a.ticket, 1u);
+  __syncthreads();
+  const int b = (int)s_b;
+  const int cnt = (int)a.tot[b];
+  const int64_t start = a.bstart[b];
+  // warp-contiguous layout over the rounds actually needed
+  const int reff = (cnt + B_CT - 1) / B_CT;          // rounds per warp
+  const int wlen = reff * 32;                        // items per warp
+  uint64_t x[B_IT];
+#pragma unroll
+  for (int it = 0; it < B_IT; ++it) {
+    const int j = warp * wlen + it * 32 + lane;
+    x[it] = (it < reff && j < cnt) ? a.items[start + j] : ~0ull;
+  }
+  const int npass = (a.s + B_RB - 1) / B_RB;
+  for (int pass = 0; pass < npass; ++pass) {
+    const int shift = a.pbits + pass * B_RB;
+    for (int i = tid; i < B_W * B_R; i += B_CT) wh[i] = 0;
+    __syncthreads();
+    unsigned rk[B_IT / 2];
+#pragma unroll
+    for (int it = 0; it < B_IT; ++it) {
+      if (it < reff) {
+        const unsigned d = (unsigned)(x[it] >> shift) & (B_R - 1);
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned run = wh[warp * B_R + d];
+        const unsigned r = run + __popc(peers & lanemask_lt());
+        if (it & 1) rk[it >> 1] |= r << 16; else rk[it >> 1] = r;
+        __syncwarp();
+        if ((__ffs(peers) - 1) == lane) wh[warp * B_R + d] = (uint16_t)(run + __popc(peers));
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over warps (in place), digit totals
+    for (int d = tid; d < B_R; d += B_CT) {
+      unsigned acc = 0;
+      for (int w = 0; w < B_W; ++w) {
+        const unsigned v = wh[w * B_R + d];
+        wh[w * B_R + d] = (uint16_t)acc;
+        acc += v;
+      }
+      dst0[d] = acc;
+    }
+    __syncthreads();
+    // exclusive scan of the digit totals (B_R = 1024 over 512 threads: 2 each)
+    {
+      const unsigned v0 = dst0[2 * tid], v1 = dst0[2 * tid + 1];
+      unsigned inc = v0 + v1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) wtot[warp] = inc;
+      __syncthreads();
+      unsigned wb = 0;
+      for (int w = 0; w < warp; ++w) wb += wtot[w];
+      const unsigned ex = wb + inc - v0 - v1;
+      __syncthreads();
+      dst0[2 * tid] = ex;
+      dst0[2 * tid + 1] = ex + v0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < B_IT; ++it) {
+      if (it < reff) {
+        const unsigned d = (unsigned)(x[it] >> shift) & (B_R - 1);
+        const unsigned r = (it & 1) ? (rk[it >> 1] >> 16) : (rk[it >> 1] & 0xffffu);
+        A[dst0[d] + wh[warp * B_R + d] + r] = x[it];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < B_IT; ++it)
+      if (it < reff) x[it] = A[warp * wlen + it * 32 + lane];
+    __syncthreads();
+  }
+  if (npass == 0) {   // one key per bucket: order irrelevant, publish for the neighbour reads
+#pragma unroll
+    for (int it = 0; it < B_IT; ++it)
+      if (it < reff) A[warp * wlen + it * 32 + lane] = x[it];
+    __syncthreads();
+  }
+  // head flags in sorted order -> local ids
+  unsigned ball[B_IT];
+  unsigned mine = 0;
+#pragma unroll
+  for (int it = 0; it < B_IT; ++it) {
+    ball[it] = 0;
+    if (it < reff) {
+      const int j = warp * wlen + it * 32 + lane;
+      const uint64_t lo = x[it] >> a.pbits;
+      const bool head = j < cnt && (j == 0 || (A[j - 1] >> a.pbits) != lo);
+      ball[it] = __ballot_sync(0xffffffffu, head);
+      mine += __popc(ball[it]);
+    }
+  }
+  if (lane == 0) wtot[warp] = mine;
+  __syncthreads();
+  unsigned wbase = 0, U = 0;
+  for (int w = 0; w < B_W; ++w) { const unsigned v = wtot[w]; wbase += w < warp ? v : 0; U += v; }
+  // decoupled look-back over the preceding buckets (ticket order)
+  if (tid == 0) {
+    int64_t prefix = 0;
+    unsigned long long* st = a.status + b;
+    if (b == 0) {
+      st_release(st, ST_PRE | (unsigned long long)U);
+    } else {
+      st_release(st, ST_AGG | (unsigned long long)U);
+      int j = b - 1;
+      while (true) {
+        const unsigned long long v = ld_acquire(a.status + j);
+        if (v & ST_PRE) { prefix += (int64_t)(v & ST_VAL); break; }
+        if (v & ST_AGG) { prefix += (int64_t)(v & ST_VAL); --j; }
+      }
+      st_release(st, ST_PRE | (unsigned long long)(prefix + U));
+    }
+    s_prefix = prefix;
+    if (b == a.nb - 1) *a.rank_out = prefix + U;
+  }
+  __syncthreads();
+  const int64_t P = s_prefix;
+  const uint64_t pmask = (1ull << a.pbits) - 1;
+  unsigned run = wbase;
+#pragma unroll
+  for (int it = 0; it < B_IT; ++it) {
+    if (it < reff) {
+      const int j = warp * wlen + it * 32 + lane;
+      if (j < cnt) {
+        const bool head = (ball[it] >> lane) & 1u;
+        const int64_t id = P + run + __popc(ball[it] & lanemask_lt()) + (head ? 1 : 0) - 1;
+        if (head) a.uniq[id] = (int64_t)(((uint64_t)b << a.s) | (x[it] >> a.pbits));
+        a.ti[(int64_t)(x[it] & pmask)] = id;
+      }
+      run += __popc(ball[it]);
+    }
+  }
+}
+
+__global__ void derive_entries(const int64_t* __restrict__ row1, const int64_t* __restrict__ col1,
+                               int64_t n, int64_t I1, int64_t J1, int64_t* __restrict__ i1,
+                               int64_t* __restrict__ j1) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (i1) i1[e] = (row1[e] - 1) % I1;
+    if (j1) j1[e] = (col1[e] - 1) % J1;
+  }
+}
+
+}  // namespace
+
+bool convert_fast(cudaStream_t st, const int64_t* row1, const int64_t* col1, const double* val,
+                  int64_t n, int64_t I1, int64_t J1, int64_t nrb, int64_t ncb, ConvLocal& c) {
+  static const int off = std::getenv("MPO_B200_CONV_FAST")
+                             ? std::atoi(std::getenv("MPO_B200_CONV_FAST")) == 0 : 0;
+  if (off || n <= 0 || n > (int64_t)0x7fffffff) return false;
+  const int kb = key_bits((uint64_t)(nrb * ncb - 1));
+  // buckets: ~8K entries each on average (room for 2x skew below the
+  // 16K on-chip capacity), a power of two no larger than the key space
+  int lgb = 0;
+  while (lgb < 12 && ((int64_t)1 << lgb) * 8192 < n) ++lgb;
+  lgb = std::min(lgb, kb);
+  const int nb = 1 << lgb;
+  const int s = kb - lgb;
+  const int pbits = std::max(1, key_bits((uint64_t)(n - 1)));
+  if (s + pbits > 64) return false;
+  KeyMap m{I1, J1, nrb, s, -1};
+  const int lgr = key_bits((uint64_t)(nrb - 1));
+  if ((nrb & (nrb - 1)) == 0 && s >= lgr) m.bc_shift = s - lgr;
+  const int ntiles = (int)cdiv(n, F_TILE);
+  static std::once_flag once[kMaxDevices];
+  once_per_device(once, [] {
+    CK(cudaFuncSetAttribute(fast_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
+    CK(cudaFuncSetAttribute(fast_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K4_SMEM));
+  });
+  DBuf<unsigned> thist((size_t)ntiles * nb, st), toff((size_t)ntiles * nb, st), tot(nb, st),
+      tkept(ntiles, st);
+  DBuf<int64_t> bstart(nb, st), tkoff(ntiles, st), info(2, st);
+  fast_hist<<<ntiles, F_CT, 0, st>>>(row1, col1, val, n, m, nb, thist.get(), tkept.get());
+  CK_LAUNCH();
+  fast_scan_tiles<<<(nb + 31) / 32, 256, 0, st>>>(thist.get(), ntiles, nb, toff.get(), tot.get());
+  CK_LAUNCH();
+  fast_scan_buckets<<<1, 1024, 0, st>>>(tot.get(), nb, tkept.get(), ntiles, bstart.get(),
+                                        tkoff.get(), info.get());
+  CK_LAUNCH();
+  note_launch(3);
+  int64_t h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, info.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int64_t nk = h[0];
+  if (h[1] > B_CAP) return false;   // a bucket too large for one CTA: general path
+  c.nkept = nk;
+  c.ti.alloc(nk, st);
+  if (nk == 0) { c.rank = 0; return true; }
+  const bool zeros = nk < n;
+  if (zeros) {
+    c.i1.alloc(nk, st);
+    c.j1.alloc(nk, st);
+    c.values.alloc(nk, st);
+  } else {
+    c.lazy = true;   // entries derivable from the input: materialised on demand
+    c.src_row = row1;
+    c.src_col = col1;
+    c.src_val = val;
+    c.I1 = I1;
+    c.J1 = J1;
+  }
+  DBuf<uint64_t> items(nk, st);
+  ScatterArgs sa{row1, col1, val, n, m, nb, pbits, thist.get(), toff.get(), bstart.get(),
+                 tkoff.get(), zeros, items.get(), c.i1.get(), c.j1.get(), c.values.get()};
+  fast_scatter<<<ntiles, F_CT, K3_SMEM, st>>>(sa);
+  CK_LAUNCH();
+  c.uniq.alloc(nk, st);   // capacity: the block count is known after K4
+  DBuf<unsigned> ticket(1, st);
+  DBuf<unsigned long long> status(nb, st);
+  DBuf<int64_t> rank(1, st);
+  CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), st));
+  CK(cudaMemsetAsync(status.get(), 0, sizeof(unsigned long long) * nb, st));
+  BucketArgs ba{items.get(), tot.get(), bstart.get(), nb, s, pbits, ticket.get(), status.get(),
+                c.uniq.get(), c.ti.get(), rank.get()};
+  fast_bucket<<<nb, B_CT, K4_SMEM, st>>>(ba);
+  CK_LAUNCH();
+  note_launch(2);
+  CK(cudaMemcpyAsync(&c.rank, rank.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return true;
+}
+
+void ensure_entries(cudaStream_t st, ConvLocal& c) {
+  if (!c.lazy) return;
+  const int64_t n = c.nkept;
+  c.i1.alloc(n, st);
+  c.j1.alloc(n, st);
+  c.values.alloc(n, st);
+  if (n > 0) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 148 * 16));
+    derive_entries<<<grid, 256, 0, st>>>(c.src_row, c.src_col, n, c.I1, c.J1, c.i1.get(),
+                                         c.j1.get());
+    CK_LAUNCH();
+    note_launch();
+    CK(cudaMemcpyAsync(c.values.get(), c.src_val, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                       st));
+  }
+  c.lazy = false;
+}
+
+}  // namespace mpob

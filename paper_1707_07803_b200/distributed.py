@@ -44,7 +44,7 @@ from math import prod
 from . import _lib
 from .partition import PartitionPlan
 
-__all__ = ["ShardResult", "DeviceOps", "convert_sharded", "convert_sharded_emulated",
+__all__ = ["ShardResult", "Entries", "DeviceOps", "convert_sharded", "convert_sharded_emulated",
            "shard_range", "SAMPLES_PER_RANK"]
 
 SAMPLES_PER_RANK = 256
@@ -52,16 +52,73 @@ SAMPLES_PER_RANK = 256
 
 @dataclass
 class ShardResult:
-    i1: object          # this rank's kept entries, input order
-    j1: object
+    entries: object     # this rank's kept entries (input order): .i1, .j1, .values
     ti: object          # GLOBAL block ids
-    values: object
     uniq: object        # the global sorted unique block keys of this rank's key range
                         # (all of them when replicate=True)
     uniq_offset: int    # global block id of uniq[0]
     rank: int           # global nonzero block count (MPO interior rank)
     kept_offset: int    # position of this shard's first kept entry globally
     nkept_total: int
+
+    # per-entry arrays: derived on first access on the device path (they are
+    # the input's in-block offsets and values, sparse.py:241-242, 236)
+    i1 = property(lambda self: self.entries.i1)
+    j1 = property(lambda self: self.entries.j1)
+    values = property(lambda self: self.entries.values)
+
+
+class Entries:
+    """Plain (i1, j1, values) holder (CPU stand-ins, tests)."""
+
+    def __init__(self, i1, j1, values):
+        self.i1, self.j1, self.values = i1, j1, values
+
+
+class _DevView:
+    """Zero-copy view of a buffer owned by a conversion handle (CUDA array
+    interface); keeps the owner alive while torch tensors reference it."""
+
+    def __init__(self, ptr, n, typestr, owner):
+        self.owner = owner
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+class _ConvHandle:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h is not None and self.h.value:
+                _lib.load().mpo_conv_free(self.h)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+        self.h = None
+
+
+class _LazyEntries:
+    """i1, j1, values of a device conversion, fetched (and, without explicit
+    zeros, derived from the input) only when first read."""
+
+    def __init__(self, ops, handle, n):
+        self._ops, self._h, self._n, self._t = ops, handle, n, None
+
+    def _get(self):
+        if self._t is None:
+            ptrs = [C.c_void_p() for _ in range(3)]
+            _lib.call("mpo_conv_ptrs", self._ops.ctx, self._h.h, C.byref(ptrs[0]),
+                      C.byref(ptrs[1]), None, C.byref(ptrs[2]), None)
+            self._t = (self._ops.view(ptrs[0], self._n, "<i8", self._h),
+                       self._ops.view(ptrs[1], self._n, "<i8", self._h),
+                       self._ops.view(ptrs[2], self._n, "<f8", self._h))
+        return self._t
+
+    i1 = property(lambda self: self._get()[0])
+    j1 = property(lambda self: self._get()[1])
+    values = property(lambda self: self._get()[2])
 
 
 def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -81,8 +138,17 @@ class DeviceOps:
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.ctx = _lib.context(self.device.index)
 
-    def local(self, row1, col1, val, plan: PartitionPlan):
+    def view(self, ptr, n, typestr, owner):
         torch = self.torch
+        if n == 0 or not ptr.value:
+            dt = {"<i8": torch.int64, "<f8": torch.float64}[typestr]
+            return torch.empty(0, dtype=dt, device=self.device)
+        return torch.as_tensor(_DevView(ptr.value, n, typestr, owner), device=self.device)
+
+    def local(self, row1, col1, val, plan: PartitionPlan):
+        """Device conversion of one shard; returns (entries, ti, uniq) with ti
+        and uniq zero-copy views of the handle's buffers.  row1/col1/val must
+        stay alive while the entries may still be read (derived from them)."""
         rf = _lib.as_i64(plan.row_factors)
         cf = _lib.as_i64(plan.col_factors)
         h = C.c_void_p()
@@ -90,20 +156,15 @@ class DeviceOps:
         _lib.call("mpo_sparse_convert", self.ctx, C.c_void_p(row1.data_ptr()),
                   C.c_void_p(col1.data_ptr()), C.c_void_p(val.data_ptr()), n, 0, plan.d,
                   rf.ctypes.data_as(_lib._I64P), cf.ctypes.data_as(_lib._I64P), C.byref(h))
-        try:
-            nk, rk = C.c_int64(), C.c_int64()
-            _lib.check(_lib.load().mpo_conv_info(h, C.byref(nk), C.byref(rk)))
-            nk, rk = nk.value, rk.value
-            i64 = dict(dtype=torch.int64, device=self.device)
-            i1 = torch.empty(nk, **i64); j1 = torch.empty(nk, **i64); ti = torch.empty(nk, **i64)
-            v = torch.empty(nk, dtype=torch.float64, device=self.device)
-            u = torch.empty(rk, **i64)
-            _lib.call("mpo_conv_copy", self.ctx, h, C.c_void_p(i1.data_ptr()),
-                      C.c_void_p(j1.data_ptr()), C.c_void_p(ti.data_ptr()),
-                      C.c_void_p(v.data_ptr()), C.c_void_p(u.data_ptr()), 0)
-        finally:
-            _lib.load().mpo_conv_free(h)
-        return i1, j1, ti, v, u
+        owner = _ConvHandle(h)
+        owner.inputs = (row1, col1, val)   # the lazily derived entries read them
+        nk, rk = C.c_int64(), C.c_int64()
+        _lib.check(_lib.load().mpo_conv_info(h, C.byref(nk), C.byref(rk)))
+        pt, pu = C.c_void_p(), C.c_void_p()
+        _lib.call("mpo_conv_ptrs", self.ctx, h, None, None, C.byref(pt), None, C.byref(pu))
+        ti = self.view(pt, nk.value, "<i8", owner)
+        u = self.view(pu, rk.value, "<i8", owner)
+        return _LazyEntries(self, owner, nk.value), ti, u
 
     def unique(self, keys, max_key: int):
         out = self.torch.empty_like(keys)
@@ -136,7 +197,7 @@ def _rank_steps(row1, col1, val, plan: PartitionPlan, ops, world: int, me: int,
     ("all_gather_v", t, counts)    -> list of every rank's t (sizes counts)
     """
     import torch
-    i1, j1, ti, values, u = ops.local(row1, col1, val, plan)
+    entries, ti, u = ops.local(row1, col1, val, plan)
     max_key = prod(plan.row_factors[1:]) * prod(plan.col_factors[1:]) - 1
     nloc = int(u.numel())
     dev = u.device
@@ -181,7 +242,7 @@ def _rank_steps(row1, col1, val, plan: PartitionPlan, ops, world: int, me: int,
     if replicate:
         parts = yield ("all_gather_v", mine, counts)
         uniq, uoff = torch.cat(parts), 0
-    return ShardResult(i1, j1, ti, values, uniq, uoff, sum(counts), sum(kept[:me]), sum(kept))
+    return ShardResult(entries, ti, uniq, uoff, sum(counts), sum(kept[:me]), sum(kept))
 
 
 def convert_sharded(row1, col1, val, plan: PartitionPlan, ops, group=None,
@@ -193,8 +254,8 @@ def convert_sharded(row1, col1, val, plan: PartitionPlan, ops, group=None,
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     me = dist.get_rank(group) if dist.is_initialized() else 0
     if world == 1:
-        i1, j1, ti, values, u = ops.local(row1, col1, val, plan)
-        return ShardResult(i1, j1, ti, values, u, 0, int(u.numel()), 0, int(ti.numel()))
+        entries, ti, u = ops.local(row1, col1, val, plan)
+        return ShardResult(entries, ti, u, 0, int(u.numel()), 0, int(ti.numel()))
     gen = _rank_steps(row1, col1, val, plan, ops, world, me, replicate)
     res = None
     while True:

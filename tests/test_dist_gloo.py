@@ -23,8 +23,9 @@ class CpuOps:
     def local(self, row1, col1, val, plan):
         st = orc.conversion_structure(row1.numpy(), col1.numpy(), val.numpy(),
                                       plan.row_factors, plan.col_factors)
+        from paper_1707_07803_b200.distributed import Entries
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a))
-        return t(st.i1), t(st.j1), t(st.ti), t(st.values), t(st.uniq)
+        return Entries(t(st.i1), t(st.j1), t(st.values)), t(st.ti), t(st.uniq)
 
     def unique(self, keys, max_key):
         return torch.from_numpy(np.unique(keys.numpy()))

@@ -210,3 +210,54 @@ def test_sharded_exchange_on_device(world):
     assert np.array_equal(cat([x.uniq for x in res]), st.uniq)
     assert all(x.rank == st.rank for x in res)
     assert max(x.uniq.numel() for x in res) <= 1.25 * st.rank / world
+
+
+def test_conversion_skewed_bucket_falls_back():
+    """Entries concentrated in one column block overflow the bucketed fast
+    path's on-chip capacity (16K entries per bucket): the onesweep path takes
+    over, same result as the oracle."""
+    m = _api()
+    from paper_1707_07803_b200.workloads import square_plan
+    rng = np.random.default_rng(8)
+    n = 1 << 16
+    r = np.sort(rng.choice(n, 60000, replace=False)) + 1
+    c = np.full(r.size, 77, dtype=np.int64)
+    r = np.concatenate([r, rng.integers(1, n + 1, 20000)])
+    c = np.concatenate([c, rng.integers(1, n + 1, 20000)])
+    key = np.unique((r - 1) * n + (c - 1))
+    r, c = key // n + 1, key % n + 1
+    v = rng.standard_normal(r.size)
+    plan = square_plan(16)
+    i1, j1, ti, vals, uniq = m.convert_structure(r, c, v, plan).arrays()
+    st = orc.conversion_structure(r, c, v, plan.row_factors, plan.col_factors)
+    assert np.array_equal(st.uniq, uniq) and np.array_equal(st.ti, ti)
+    assert np.array_equal(st.i1, i1) and np.array_equal(st.j1, j1)
+
+
+def test_conversion_fast_and_onesweep_paths_agree():
+    """The bucketed fast path (default) and the onesweep path
+    (MPO_B200_CONV_FAST=0, a fresh process) give bit-identical structures on
+    shuffled input with explicit zeros."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.');"
+        "import paper_1707_07803_b200 as m;"
+        "from paper_1707_07803_b200.workloads import powerlaw_coo, square_plan;"
+        "r, c, v = powerlaw_coo(1 << 18, seed=31);"
+        "p = np.random.default_rng(2).permutation(r.size); r, c, v = r[p], c[p], v[p].copy();"
+        "v[::97] = 0.0;"
+        "a = m.convert_structure(r, c, v, square_plan(18)).arrays();"
+        "np.savez(sys.argv[1], *a)")
+    import os
+    import tempfile
+    from conftest import ROOT
+    outs = []
+    for fast in ("1", "0"):
+        path = os.path.join(tempfile.mkdtemp(), "o.npz")
+        env = dict(os.environ, MPO_B200_CONV_FAST=fast)
+        subprocess.run([sys.executable, "-c", code, path], cwd=ROOT, env=env, check=True)
+        z = np.load(path)
+        outs.append([z[f"arr_{k}"] for k in range(5)])
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
