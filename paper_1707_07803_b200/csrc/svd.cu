@@ -24,8 +24,9 @@
 // Iteration stops after a sweep in which no pair needed rotating
 // (|x_p.x_q| <= tol ||x_p|| ||x_q|| for every column pair), which gives
 // singular values to O(eps ||M||) like dgesdd.  Singular values are the
-// final column norms, sorted descending with index tie-break.  No atomics,
-// fixed reduction orders: bitwise deterministic.
+// final column norms, sorted descending with index tie-break.  Fixed
+// reduction orders (the one atomic, the sweep's largest-coupling atomicMax,
+// is order-independent): bitwise deterministic.
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -137,8 +138,6 @@ struct JacArgs {
   int* skiplog;    // profiling only: per (round, pair) skip flags, or null
   int which;       // apply: 0 = X, 1 = V
   int cross;       // eig: rotate only the cross-block pairs (NPR inner rounds)
-  float* X32;      // TF32 preconditioning phase: FP32 copies of X and V
-  float* V32;
 };
 
 template <int JB>
@@ -730,213 +729,6 @@ __global__ void __launch_bounds__(JT, 2) jacobi_apply_kernel(JacArgs a) {
   }
 }
 
-// ---- FP32 preconditioning phase (mixed-precision Jacobi) -----------------
-// The first sweeps of a large Jacobi only need rotations to FP32 accuracy:
-// they run on FP32 copies of X and V with the Gram and the J products as
-// 3xTF32 on the TF32 tensor pipe (mma.sync m16n8k8, FP32 accumulate; 278
-// TFLOP/s measured vs 37 for FP64 DMMA, and half the bytes).  The eig kernel is the
-// FP64 one, unchanged (it reads FP64 Gram partials).  Afterwards V is
-// re-orthonormalised in FP64 (Newton-Schulz), X <- X0 V in FP64, and the
-// FP64 sweeps continue from there to the full convergence test: accuracy
-// is decided only by the FP64 phase.
-constexpr int LDG32 = CH + 4;   // gram chunk column stride (floats): conflict-free A/B fragments
-constexpr int LDA32 = CH + 8;   // apply chunk column stride (floats)
-
-__device__ __forceinline__ unsigned to_tf32(float x) {
-  unsigned r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], unsigned b0,
-                                         unsigned b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};\n"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-// 3xTF32: x = hi + lo with hi, lo TF32-representable; a product is
-// hi*hi + hi*lo + lo*hi (the lo*lo term is below FP32 rounding), which gives
-// FP32-level accuracy on the TF32 pipe
-__device__ __forceinline__ void split_tf32(float x, unsigned& hi, unsigned& lo) {
-  hi = to_tf32(x);
-  lo = to_tf32(x - __uint_as_float(hi));
-}
-
-// cp.async loader of CH rows of the pair's P2 columns of an FP32 matrix into
-// a column-major chunk with stride LD (16-byte segments of 4 rows)
-template <int JB, int LD>
-struct ChunkLoader32 {
-  static constexpr int P2 = 2 * JB, SEGC = CH / 4, NSEG = P2 * SEGC, PER = (NSEG + JT - 1) / JT;
-  const float* src[PER];
-  int dst[PER];
-  int r4[PER];
-  bool on[PER];
-  __device__ __forceinline__ ChunkLoader32(const float* M, int64_t ld, int bx, int by) {
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      const int sidx = threadIdx.x + j * JT;
-      on[j] = sidx < NSEG;
-      const int c = on[j] ? sidx / SEGC : 0, seg = sidx % SEGC;
-      r4[j] = 4 * seg;
-      src[j] = M + gcol<JB>(c, bx, by) * ld + r4[j];
-      dst[j] = c * LD + r4[j];
-    }
-  }
-  __device__ __forceinline__ void load(float* buf, int64_t r0, int64_t rend) const {
-#pragma unroll
-    for (int j = 0; j < PER; ++j)
-      if (on[j]) {
-        const bool ok = r0 + r4[j] < rend;
-        cp_async16(buf + dst[j], src[j] + (ok ? r0 : 0), ok ? 16 : 0);
-      }
-  }
-};
-
-// partial P2 x P2 Gram of the pair's FP32 columns over this CTA's rows, TF32
-// products, FP32 accumulation, written as FP64 (full matrix) for the eig
-template <int JB>
-__global__ void __launch_bounds__(JT) jacobi_gram_tf32_kernel(JacArgs a) {
-  constexpr int P2 = 2 * JB, MT = P2 / 16, NT8 = P2 / 8, TILES = MT * NT8, TPW = TILES / 8;
-  __shared__ __align__(16) float buf[2][P2 * LDG32];
-  const int pair = blockIdx.x, split = blockIdx.y;
-  int bx, by;
-  pair_of_round(a.nb, a.round, pair, bx, by);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, tq = lane & 3;
-  const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
-  const int mt = warp % MT, nt0 = (warp / MT) * TPW;
-  float acc[TPW][4];
-#pragma unroll
-  for (int u = 0; u < TPW; ++u) acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0.f;
-  const int nch = (int)cdiv_dev(re - rb, CH);
-  const ChunkLoader32<JB, LDG32> ldr(a.X32, a.ld, bx, by);
-  if (nch > 0) ldr.load(buf[0], rb, re);
-  cp_async_commit();
-  for (int i = 0; i < nch; ++i) {
-    if (i + 1 < nch) ldr.load(buf[(i + 1) & 1], rb + (int64_t)(i + 1) * CH, re);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const float* b = buf[i & 1];
-#pragma unroll
-    for (int k0 = 0; k0 < CH; k0 += 8) {
-      // A[m][k] = X[k][col m]: a0 (g, t) a1 (g+8, t) a2 (g, t+4) a3 (g+8, t+4)
-      const float* pa = b + (mt * 16 + g) * LDG32 + k0 + tq;
-      const float av[4] = {pa[0], pa[8 * LDG32], pa[4], pa[8 * LDG32 + 4]};
-      unsigned ah[4], al[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) split_tf32(av[e], ah[e], al[e]);
-#pragma unroll
-      for (int u = 0; u < TPW; ++u) {
-        const float* pb = b + ((nt0 + u) * 8 + g) * LDG32 + k0 + tq;
-        unsigned bh0, bl0, bh1, bl1;
-        split_tf32(pb[0], bh0, bl0);
-        split_tf32(pb[4], bh1, bl1);
-        mma_tf32(acc[u], al, bh0, bh1);
-        mma_tf32(acc[u], ah, bl0, bl1);
-        mma_tf32(acc[u], ah, bh0, bh1);
-      }
-    }
-    __syncthreads();
-  }
-  double* G = a.gpart + ((int64_t)pair * a.splits + split) * (P2 * P2);
-#pragma unroll
-  for (int u = 0; u < TPW; ++u) {
-    const int gi = mt * 16 + g, gj = (nt0 + u) * 8 + 2 * tq;
-    G[gi * P2 + gj] = acc[u][0];
-    G[gi * P2 + gj + 1] = acc[u][1];
-    G[(gi + 8) * P2 + gj] = acc[u][2];
-    G[(gi + 8) * P2 + gj + 1] = acc[u][3];
-  }
-}
-
-// M32[:, pair columns] <- M32[:, pair columns] J (TF32 products), this CTA's rows
-template <int JB>
-__global__ void __launch_bounds__(JT) jacobi_apply_tf32_kernel(JacArgs a) {
-  constexpr int P2 = 2 * JB, MT = CH / 16, NT8 = P2 / 8, TPW = MT * NT8 / 8, KS = P2 / 8;
-  __shared__ __align__(16) float buf[2][P2 * LDA32];
-  const int pair = blockIdx.x;
-  if (a.skip[pair]) return;
-  const int split = blockIdx.y;
-  float* M = a.which == 0 ? a.X32 : a.V32;
-  int bx, by;
-  pair_of_round(a.nb, a.round, pair, bx, by);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, tq = lane & 3;
-  const int64_t rb = split * a.rps, re = min(a.rows, rb + a.rps);
-  const int nch = (int)cdiv_dev(re - rb, CH);
-  const ChunkLoader32<JB, LDA32> ldr(M, a.ld, bx, by);
-  if (nch > 0) ldr.load(buf[0], rb, re);
-  cp_async_commit();
-  const int mt = warp % MT, nt0 = (warp / MT) * TPW;
-  // B[k][n] = J[k][n] (row-major P2 x P2): b0 (t, g), b1 (t+4, g)
-  const double* Jg = a.J + (int64_t)pair * P2 * P2;
-  unsigned bj[TPW][KS][2], bjl[TPW][KS][2];
-#pragma unroll
-  for (int u = 0; u < TPW; ++u)
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int n = (nt0 + u) * 8 + g, k = ks * 8 + tq;
-      split_tf32((float)Jg[k * P2 + n], bj[u][ks][0], bjl[u][ks][0]);
-      split_tf32((float)Jg[(k + 4) * P2 + n], bj[u][ks][1], bjl[u][ks][1]);
-    }
-  int64_t coff[TPW][2];
-#pragma unroll
-  for (int u = 0; u < TPW; ++u)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) coff[u][e] = gcol<JB>((nt0 + u) * 8 + 2 * tq + e, bx, by) * a.ld;
-  for (int i = 0; i < nch; ++i) {
-    if (i + 1 < nch) ldr.load(buf[(i + 1) & 1], rb + (int64_t)(i + 1) * CH, re);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const float* b = buf[i & 1];
-    float o[TPW][4];
-#pragma unroll
-    for (int u = 0; u < TPW; ++u) o[u][0] = o[u][1] = o[u][2] = o[u][3] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      // A[m][k] = M[row m][col k]: a0 (g, t) a1 (g+8, t) a2 (g, t+4) a3 (g+8, t+4)
-      const float* pa = b + (ks * 8 + tq) * LDA32 + mt * 16 + g;
-      const float av[4] = {pa[0], pa[8], pa[4 * LDA32], pa[4 * LDA32 + 8]};
-      unsigned ah[4], al[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) split_tf32(av[e], ah[e], al[e]);
-#pragma unroll
-      for (int u = 0; u < TPW; ++u) {
-        mma_tf32(o[u], al, bj[u][ks][0], bj[u][ks][1]);
-        mma_tf32(o[u], ah, bjl[u][ks][0], bjl[u][ks][1]);
-        mma_tf32(o[u], ah, bj[u][ks][0], bj[u][ks][1]);
-      }
-    }
-    const int64_t r0 = rb + (int64_t)i * CH + mt * 16 + g;
-#pragma unroll
-    for (int u = 0; u < TPW; ++u) {
-      M[r0 + coff[u][0]] = o[u][0];
-      M[r0 + coff[u][1]] = o[u][1];
-      M[r0 + 8 + coff[u][0]] = o[u][2];
-      M[r0 + 8 + coff[u][1]] = o[u][3];
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void f64_to_f32_kernel(const double* __restrict__ x, float* __restrict__ y, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = (float)x[i];
-}
-__global__ void f32_to_f64_kernel(const float* __restrict__ x, double* __restrict__ y, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = (double)x[i];
-}
-__global__ void identity32_kernel(float* A, int64_t n) {
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n * n;
-       idx += (int64_t)gridDim.x * blockDim.x)
-    A[idx] = (idx % n == idx / n) ? 1.f : 0.f;
-}
-
 // per-column norms (one warp per column, fixed reduction order)
 __global__ void col_norms_kernel(const double* X, int64_t rows, int64_t ld, int64_t ncols,
                                  double* out) {
@@ -1125,7 +917,7 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
   DBuf<unsigned> cmaxb(1, st);
   JacArgs a{X, V, kp, kp, nb, 0, splits, rps, gpart.get(), Jb[0], Sb[0], flag.get(), cmaxb.get(), tol,
             fro.get(), noise_floor ? floor_c * floor_c : 0.0, inner, ns_steps,
-            nullptr, 0, 0, nullptr, nullptr};
+            nullptr, 0, 0};
   // profiling (bench.py roofline): CUDA events around every round kernel;
   // the V updates then stay on the main stream so the intervals are exact
   const bool prof = g_prof.on;
@@ -1173,95 +965,6 @@ static int jacobi_sweeps(cudaStream_t st, double* X, int64_t k, int64_t kp, doub
     nrm.alloc(kp, st);
     prm.alloc(kp, st);
     sort_smem_attr();
-  }
-  // mixed precision: FP32 (3xTF32) preconditioning sweeps on FP32 copies of
-  // X and V (kernels above), then V re-orthonormalised in FP64 and
-  // X <- X0 V; the FP64 sweeps below start from there
-  static const int mp_on =
-      std::getenv("MPO_B200_MP") ? std::atoi(std::getenv("MPO_B200_MP")) : 0;
-  static const int64_t mp_mink =
-      std::getenv("MPO_B200_MP_MINK") ? std::atoll(std::getenv("MPO_B200_MP_MINK")) : 1536;
-  static const int mp_sweeps =
-      std::getenv("MPO_B200_MP_SWEEPS") ? std::atoi(std::getenv("MPO_B200_MP_SWEEPS")) : 20;
-  static const double mp_tol =
-      std::getenv("MPO_B200_MP_TOL") ? std::atof(std::getenv("MPO_B200_MP_TOL")) : 4e-6;
-  static const int mp_ns =
-      std::getenv("MPO_B200_MP_NS") ? std::atoi(std::getenv("MPO_B200_MP_NS")) : 2;
-  if (mp_on && k >= mp_mink && !prof) {
-    DBuf<float> X32((size_t)kp * kp, st), V32((size_t)kp * kp, st);
-    f64_to_f32_kernel<<<gridn(kp * kp), 256, 0, st>>>(X, X32.get(), kp * kp);
-    CK_LAUNCH();
-    identity32_kernel<<<gridn(kp * kp), 256, 0, st>>>(V32.get(), kp);
-    CK_LAUNCH();
-    note_launch(2);
-    if (overlap) {
-      CK(cudaEventRecord(evV[0], st));
-      CK(cudaStreamWaitEvent(sv, evV[0], 0));
-      CK(cudaEventRecord(evV[1], st));
-    }
-    JacArgs b32 = a;
-    b32.X32 = X32.get();
-    b32.V32 = V32.get();
-    b32.tol = mp_tol;
-    int64_t r32 = 0;
-    int s32 = 0;
-    for (; s32 < mp_sweeps; ++s32) {
-      CK(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
-      for (int r = 0; r < nb - 1; ++r, ++r32) {
-        const int par = (int)(r32 & 1);
-        b32.round = r;
-        b32.cross = cross_from >= 0 && s32 >= cross_from && r > 0;
-        b32.J = Jb[par];
-        b32.skip = Sb[par];
-        jacobi_gram_tf32_kernel<JB><<<dim3(npairs, splits), JT, 0, st>>>(b32);
-        CK_LAUNCH();
-        if (overlap) CK(cudaStreamWaitEvent(st, evV[par], 0));
-        jacobi_eig_kernel<JB><<<npairs, K::ET, eig_smem<JB>(), st>>>(b32);
-        CK_LAUNCH();
-        if (overlap) CK(cudaEventRecord(evE[par], st));
-        b32.which = 0;
-        jacobi_apply_tf32_kernel<JB><<<dim3(npairs, splits), JT, 0, st>>>(b32);
-        CK_LAUNCH();
-        b32.which = 1;
-        if (overlap) CK(cudaStreamWaitEvent(sv, evE[par], 0));
-        jacobi_apply_tf32_kernel<JB><<<dim3(npairs, splits), JT, 0, sv>>>(b32);
-        CK_LAUNCH();
-        if (overlap) CK(cudaEventRecord(evV[par], sv));
-      }
-      note_launch(4 * (nb - 1));
-      int hf = 0;
-      CK(cudaMemcpyAsync(&hf, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      if (!hf) { ++s32; break; }
-    }
-    if (overlap) {
-      CK(cudaEventRecord(evV[0], sv));
-      CK(cudaStreamWaitEvent(st, evV[0], 0));
-    }
-    // V <- orthonormalised V32 (Newton-Schulz in FP64), X <- X0 V
-    f32_to_f64_kernel<<<gridn(kp * kp), 256, 0, st>>>(V32.get(), V, kp * kp);
-    CK_LAUNCH();
-    note_launch();
-    X32.reset();
-    V32.reset();
-    {
-      DBuf<double> E((size_t)kp * kp, st), VE((size_t)kp * kp, st);
-      for (int it = 0; it < mp_ns; ++it) {
-        set_identity(st, kp, kp, E.get(), kp);
-        dgemm(st, true, false, kp, kp, kp, 1.0, V, kp, V, kp, -1.0, E.get(), kp);
-        dgemm(st, false, false, kp, kp, kp, 1.0, V, kp, E.get(), kp, 0.0, VE.get(), kp);
-        dgemm_axpy(st, kp * kp, -0.5, VE.get(), V);
-      }
-      dgemm(st, false, false, kp, kp, kp, 1.0, X0, kp, V, kp, 0.0, X, kp);
-    }
-    if (overlap) {
-      for (int i = 0; i < 2; ++i) CK(cudaEventRecord(evV[i], st));
-      CK(cudaStreamWaitEvent(sv, evV[0], 0));
-    }
-    if (trace_lvl) {
-      CK(cudaStreamSynchronize(st));
-      fprintf(stderr, "[mpo_b200]     k=%lld fp32 preconditioning: %d sweeps\n", (long long)k, s32);
-    }
   }
   int h_flag = 0, sweeps = 0;
   int64_t rr = 0;   // global round counter (buffer parity across sweeps)
