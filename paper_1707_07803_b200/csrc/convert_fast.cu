@@ -14,7 +14,7 @@
 //                                                              write 8 B / entry
 //   K4 fast_bucket   per bucket (<= 16K entries, taken in bucket order from a
 //                    ticket): stable LSD sort of the low key bits on chip
-//                    (10-bit digits, warp-private counters + __match_any),
+//                    (10-bit digits, warp-private counters + ballot multisplit),
 //                    head flags -> local block ids, decoupled look-back over
 //                    the preceding buckets for the global id offset, then
 //                    uniq (coalesced) and ti[position]        read 8 B, write
@@ -63,23 +63,44 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// x / d without a 64-bit division: a shift for powers of two, a 32-bit
+// division when both fit (row/col indices below 2^32)
+struct FastDiv {
+  uint64_t d;
+  int sh;   // >= 0: power of two
+};
+FastDiv make_div(int64_t d) {
+  FastDiv f{(uint64_t)d, -1};
+  if ((d & (d - 1)) == 0) { f.sh = 0; while (((uint64_t)1 << f.sh) < (uint64_t)d) ++f.sh; }
+  return f;
+}
+__device__ __forceinline__ uint64_t fdiv(const FastDiv& f, uint64_t x) {
+  if (f.sh >= 0) return x >> f.sh;
+  if ((x >> 32) == 0 && (f.d >> 32) == 0) return (uint32_t)x / (uint32_t)f.d;
+  return x / f.d;
+}
+
 struct KeyMap {
-  int64_t I1, J1, nrb;
+  FastDiv I1, J1;
+  int64_t nrb;
   int s;          // bucket = key >> s
   int bc_shift;   // >= 0: bucket = bc >> bc_shift (no row needed); -1: full key
 };
 
 __device__ __forceinline__ uint64_t entry_key(const KeyMap& m, int64_t r1, int64_t c1) {
-  const int64_t br = (r1 - 1) / m.I1, bc = (c1 - 1) / m.J1;
-  return (uint64_t)(br + m.nrb * bc);
+  const uint64_t br = fdiv(m.I1, (uint64_t)(r1 - 1)), bc = fdiv(m.J1, (uint64_t)(c1 - 1));
+  return br + (uint64_t)m.nrb * bc;
 }
 
 // ---------------- K1 -------------------------------------------------------
-__global__ void __launch_bounds__(F_CT) fast_hist(const int64_t* __restrict__ row1,
+__global__ void __launch_bounds__(F_CT, 2) fast_hist(const int64_t* __restrict__ row1,
                                                   const int64_t* __restrict__ col1,
                                                   const double* __restrict__ val, int64_t n,
-                                                  KeyMap m, int nb, unsigned* __restrict__ thist,
+                                                  KeyMap m, int nb, bool zero_aware,
+                                                  unsigned* __restrict__ thist,
                                                   unsigned* __restrict__ tkept) {
+  // zero_aware = false: every entry counted as kept (fast_scatter checks the
+  // values and flags a rerun with zero_aware = true if any is zero)
   __shared__ unsigned h[F_MAXB];
   __shared__ unsigned wsum[F_CT / 32];
   for (int i = threadIdx.x; i < nb; i += F_CT) h[i] = 0;
@@ -97,14 +118,14 @@ __global__ void __launch_bounds__(F_CT) fast_hist(const int64_t* __restrict__ ro
       const int64_t i = base + (it0 + u) * F_CT + threadIdx.x;
       const bool ok = i < n;
       cv[u] = ok ? col1[i] : 1;
-      vv[u] = ok ? val[i] : 0.0;
+      vv[u] = ok ? (zero_aware ? val[i] : 1.0) : 0.0;
       rv[u] = (ok && m.bc_shift < 0) ? row1[i] : 1;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (vv[u] != 0.0) {
         unsigned b;
-        if (m.bc_shift >= 0) b = (unsigned)(((cv[u] - 1) / m.J1) >> m.bc_shift);
+        if (m.bc_shift >= 0) b = (unsigned)(fdiv(m.J1, (uint64_t)(cv[u] - 1)) >> m.bc_shift);
         else b = (unsigned)(entry_key(m, rv[u], cv[u]) >> m.s);
         atomicAdd(&h[b], 1u);
         ++c;
@@ -125,32 +146,54 @@ __global__ void __launch_bounds__(F_CT) fast_hist(const int64_t* __restrict__ ro
 }
 
 // ---------------- K2 -------------------------------------------------------
-// per bucket (lane), 8 warps over contiguous tile segments: tile prefix of
-// the bucket counts (toff, without the bucket start) and the bucket totals
-__global__ void __launch_bounds__(256) fast_scan_tiles(const unsigned* __restrict__ thist,
-                                                       int ntiles, int nb,
-                                                       unsigned* __restrict__ toff,
-                                                       unsigned* __restrict__ tot) {
-  __shared__ unsigned ssum[8][32];
+// per bucket (lane), 32 warps over contiguous tile segments, 8 loads in
+// flight per lane: tile prefix of the bucket counts (toff, without the
+// bucket start) and the bucket totals
+__global__ void __launch_bounds__(1024) fast_scan_tiles(const unsigned* __restrict__ thist,
+                                                        int ntiles, int nb,
+                                                        unsigned* __restrict__ toff,
+                                                        unsigned* __restrict__ tot) {
+  __shared__ unsigned ssum[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x * 32 + lane;
-  const int seg = (ntiles + 7) / 8;
+  const int seg = (ntiles + 31) / 32;
   const int t0 = warp * seg, t1 = min(ntiles, t0 + seg);
+  constexpr int U = 8;
   unsigned s = 0;
-  if (b < nb)
-    for (int t = t0; t < t1; ++t) s += thist[(int64_t)t * nb + b];
+  if (b < nb) {
+    int t = t0;
+    for (; t + U <= t1; t += U) {
+      unsigned v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = thist[(int64_t)(t + u) * nb + b];
+#pragma unroll
+      for (int u = 0; u < U; ++u) s += v[u];
+    }
+    for (; t < t1; ++t) s += thist[(int64_t)t * nb + b];
+  }
   ssum[warp][lane] = s;
   __syncthreads();
   unsigned run = 0;
   for (int w = 0; w < warp; ++w) run += ssum[w][lane];
   if (b < nb) {
-    for (int t = t0; t < t1; ++t) {
+    int t = t0;
+    for (; t + U <= t1; t += U) {
+      unsigned v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = thist[(int64_t)(t + u) * nb + b];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        toff[(int64_t)(t + u) * nb + b] = run;
+        run += v[u];
+      }
+    }
+    for (; t < t1; ++t) {
       const int64_t o = (int64_t)t * nb + b;
       const unsigned v = thist[o];
       toff[o] = run;
       run += v;
     }
-    if (warp == 7) tot[b] = run;
+    if (warp == 31) tot[b] = run;
   }
 }
 
@@ -213,6 +256,7 @@ struct ScatterArgs {
   const int64_t* bstart;
   const int64_t* tkoff;
   bool zeros;          // explicit zeros present: compact, write i1/j1/values
+  int* zero_found;     // !zeros: set if a zero value turns up (rerun zero-aware)
   uint64_t* items;
   int64_t* i1;
   int64_t* j1;
@@ -266,43 +310,58 @@ __global__ void __launch_bounds__(F_CT) fast_scatter(ScatterArgs a) {
   const int64_t base = blockIdx.x * (int64_t)F_TILE;
   int64_t kbase = a.zeros ? a.tkoff[blockIdx.x] : base;
   const uint64_t lowmask = a.m.s >= 64 ? ~0ull : ((1ull << a.m.s) - 1);
+  constexpr int U = 8;   // rounds of loads in flight
+  bool saw_zero = false;
 #pragma unroll 1
-  for (int it = 0; it < F_IT; ++it) {
-    const int64_t i = base + it * F_CT + tid;
-    const bool ok = i < a.n;
-    const int64_t r1 = ok ? a.row1[i] : 1, c1 = ok ? a.col1[i] : 1;
-    const double v = ok ? a.val[i] : 0.0;
-    const bool keep = ok && v != 0.0;
-    int64_t pos;
-    if (a.zeros) {
-      // kept index in input order: ballot + warp prefix for this round
-      const unsigned ball = __ballot_sync(0xffffffffu, keep);
-      if (lane == 0) wpart[warp] = __popc(ball);
-      __syncthreads();
-      unsigned before = 0, tot = 0;
-      for (int w = 0; w < F_CT / 32; ++w) { const unsigned x = wpart[w]; before += w < warp ? x : 0; tot += x; }
-      pos = kbase + before + __popc(ball & lanemask_lt());
-      kbase += tot;
-      __syncthreads();
-    } else {
-      pos = i;
+  for (int it0 = 0; it0 < F_IT; it0 += U) {
+    int64_t rr[U], cc[U];
+    double vv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (it0 + u) * F_CT + tid;
+      const bool ok = i < a.n;
+      rr[u] = ok ? a.row1[i] : 1;
+      cc[u] = ok ? a.col1[i] : 1;
+      vv[u] = ok ? a.val[i] : 0.0;
     }
-    if (keep) {
-      const int64_t r0 = r1 - 1, c0 = c1 - 1;
-      const int64_t br = r0 / a.m.I1, bc = c0 / a.m.J1;
-      const uint64_t key = (uint64_t)(br + a.m.nrb * bc);
-      const unsigned b = (unsigned)(key >> a.m.s);
-      const unsigned slot = atomicAdd(&cur[b], 1u);   // in-tile slot: order irrelevant
-      const unsigned j = loff[b] + slot;
-      sitem[j] = ((key & lowmask) << a.pbits) | (uint64_t)pos;
-      sb[j] = (uint16_t)b;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + (it0 + u) * F_CT + tid;
+      const bool ok = i < a.n;
+      bool keep = ok && vv[u] != 0.0;
+      int64_t pos = i;
       if (a.zeros) {
-        a.i1[pos] = r0 - br * a.m.I1;
-        a.j1[pos] = c0 - bc * a.m.J1;
-        a.values[pos] = v;
+        // kept index in input order: ballot + warp prefix for this round
+        const unsigned ball = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wpart[warp] = __popc(ball);
+        __syncthreads();
+        unsigned before = 0, tot = 0;
+        for (int w = 0; w < F_CT / 32; ++w) { const unsigned x = wpart[w]; before += w < warp ? x : 0; tot += x; }
+        pos = kbase + before + __popc(ball & lanemask_lt());
+        kbase += tot;
+        __syncthreads();
+      } else if (ok && !keep) {
+        saw_zero = true;   // counted as kept by fast_hist: the result is discarded
+        keep = true;
+      }
+      if (keep) {
+        const uint64_t r0 = (uint64_t)(rr[u] - 1), c0 = (uint64_t)(cc[u] - 1);
+        const uint64_t br = fdiv(a.m.I1, r0), bc = fdiv(a.m.J1, c0);
+        const uint64_t key = br + (uint64_t)a.m.nrb * bc;
+        const unsigned b = (unsigned)(key >> a.m.s);
+        const unsigned slot = atomicAdd(&cur[b], 1u);   // in-tile slot: order irrelevant
+        const unsigned j = loff[b] + slot;
+        sitem[j] = ((key & lowmask) << a.pbits) | (uint64_t)pos;
+        sb[j] = (uint16_t)b;
+        if (a.zeros) {
+          a.i1[pos] = (int64_t)(r0 - br * a.m.I1.d);
+          a.j1[pos] = (int64_t)(c0 - bc * a.m.J1.d);
+          a.values[pos] = vv[u];
+        }
       }
     }
   }
+  if (saw_zero) atomicOr(a.zero_found, 1);
   __syncthreads();
   // global start of this tile's run in each bucket (n < 2^31: fits 32 bits)
   const unsigned* trow = a.toff + (int64_t)blockIdx.x * nb;
@@ -318,6 +377,8 @@ struct BucketArgs {
   const unsigned* tot;
   const int64_t* bstart;
   int nb, s, pbits;
+  int gbits;   // > 0: group sort (the low key's top gbits select a group, the
+               // rest orders items inside it); 0: LSD passes over all s bits
   unsigned* ticket;
   unsigned long long* status;
   int64_t* uniq;
@@ -350,7 +411,98 @@ __global__ void __launch_bounds__(B_CT, 1) fast_bucket(BucketArgs a) {
     const int j = warp * wlen + it * 32 + lane;
     x[it] = (it < reff && j < cnt) ? a.items[start + j] : ~0ull;
   }
-  const int npass = (a.s + B_RB - 1) / B_RB;
+  // Group sort: one counting pass on the low key's top gbits (for the
+  // square 2^k plans: the block column inside the bucket) puts every
+  // block column's items together; each group (~16 items on average) is
+  // then ordered by one thread (insertion sort on the whole item, i.e. by
+  // block row, then position).  Buckets whose largest group exceeds
+  // GMAX take the LSD passes instead.
+  constexpr int GMAX = 64;
+  __shared__ int s_general;
+  bool sorted_in_A = false;
+  if (a.gbits > 0) {
+    unsigned* gh = reinterpret_cast<unsigned*>(wh);          // counts, then offsets
+    unsigned* gc = gh + (1 << a.gbits);                      // cursors
+    const int G = 1 << a.gbits;
+    const int gshift = a.pbits + a.s - a.gbits;
+    for (int g = tid; g < G; g += B_CT) { gh[g] = 0; gc[g] = 0; }
+    if (tid == 0) s_general = 0;
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < B_IT; ++it)
+      if (it < reff && warp * wlen + it * 32 + lane < cnt)
+        atomicAdd(&gh[(unsigned)(x[it] >> gshift) & (G - 1)], 1u);
+    __syncthreads();
+    // exclusive scan of the G (<= 2048) group counts, 4 per thread
+    {
+      unsigned v[4], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int g = tid * 4 + q;
+        v[q] = g < G ? gh[g] : 0u;
+        sum += v[q];
+        if (v[q] > GMAX) s_general = 1;
+      }
+      unsigned inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (lane == 31) wtot[warp] = inc;
+      __syncthreads();
+      unsigned run = inc - sum;
+      for (int w = 0; w < warp; ++w) run += wtot[w];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int g = tid * 4 + q;
+        if (g < G) gh[g] = run;
+        run += v[q];
+      }
+    }
+    __syncthreads();
+    if (!s_general) {
+#pragma unroll
+      for (int it = 0; it < B_IT; ++it)
+        if (it < reff && warp * wlen + it * 32 + lane < cnt) {
+          const unsigned g = (unsigned)(x[it] >> gshift) & (G - 1);
+          A[gh[g] + atomicAdd(&gc[g], 1u)] = x[it];
+        }
+      __syncthreads();
+      // one warp per group, rank sort: every lane counts the group's
+      // smaller items through independent shuffles (items are distinct:
+      // they carry their position) and stores its item at that rank
+      for (int g = warp; g < G; g += B_W) {
+        const unsigned lo = gh[g], n_g = gc[g];
+        if (n_g <= 1) continue;
+        if (n_g <= 32) {
+          const uint64_t v = lane < (int)n_g ? A[lo + lane] : ~0ull;
+          unsigned r = 0;
+          for (int i = 0; i < (int)n_g; ++i) r += __shfl_sync(0xffffffffu, v, i) < v;
+          if (lane < (int)n_g) A[lo + r] = v;
+        } else {
+          const uint64_t v0 = A[lo + lane];
+          const uint64_t v1 = lane + 32 < (int)n_g ? A[lo + lane + 32] : ~0ull;
+          unsigned r0 = 0, r1 = 0;
+          for (int i = 0; i < (int)n_g; ++i) {
+            const uint64_t o = i < 32 ? __shfl_sync(0xffffffffu, v0, i & 31)
+                                      : __shfl_sync(0xffffffffu, v1, i & 31);
+            r0 += o < v0;
+            r1 += o < v1;
+          }
+          A[lo + r0] = v0;
+          if (lane + 32 < (int)n_g) A[lo + r1] = v1;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int it = 0; it < B_IT; ++it)
+        if (it < reff) x[it] = A[warp * wlen + it * 32 + lane];
+      sorted_in_A = true;
+    }
+    __syncthreads();
+  }
+  const int npass = sorted_in_A ? 0 : (a.s + B_RB - 1) / B_RB;
   for (int pass = 0; pass < npass; ++pass) {
     const int shift = a.pbits + pass * B_RB;
     for (int i = tid; i < B_W * B_R; i += B_CT) wh[i] = 0;
@@ -360,7 +512,15 @@ __global__ void __launch_bounds__(B_CT, 1) fast_bucket(BucketArgs a) {
     for (int it = 0; it < B_IT; ++it) {
       if (it < reff) {
         const unsigned d = (unsigned)(x[it] >> shift) & (B_R - 1);
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        // lanes holding the same digit: AND of one ballot per digit bit
+        // (cheaper than __match_any_sync, whose latency stalled this loop)
+        unsigned peers = 0xffffffffu;
+#pragma unroll
+        for (int k = 0; k < B_RB; ++k) {
+          const bool bit = (d >> k) & 1u;
+          const unsigned bt = __ballot_sync(0xffffffffu, bit);
+          peers &= bit ? bt : ~bt;
+        }
         const unsigned run = wh[warp * B_R + d];
         const unsigned r = run + __popc(peers & lanemask_lt());
         if (it & 1) rk[it >> 1] |= r << 16; else rk[it >> 1] = r;
@@ -414,7 +574,7 @@ __global__ void __launch_bounds__(B_CT, 1) fast_bucket(BucketArgs a) {
       if (it < reff) x[it] = A[warp * wlen + it * 32 + lane];
     __syncthreads();
   }
-  if (npass == 0) {   // one key per bucket: order irrelevant, publish for the neighbour reads
+  if (npass == 0 && !sorted_in_A) {   // one key per bucket: publish for the neighbour reads
 #pragma unroll
     for (int it = 0; it < B_IT; ++it)
       if (it < reff) A[warp * wlen + it * 32 + lane] = x[it];
@@ -438,24 +598,32 @@ __global__ void __launch_bounds__(B_CT, 1) fast_bucket(BucketArgs a) {
   __syncthreads();
   unsigned wbase = 0, U = 0;
   for (int w = 0; w < B_W; ++w) { const unsigned v = wtot[w]; wbase += w < warp ? v : 0; U += v; }
-  // decoupled look-back over the preceding buckets (ticket order)
-  if (tid == 0) {
+  // decoupled look-back over the preceding buckets (ticket order), one warp
+  // reading 32 predecessors' status words per step
+  if (warp == 0) {
+    if (lane == 0) st_release(a.status + b, (b == 0 ? ST_PRE : ST_AGG) | (unsigned long long)U);
     int64_t prefix = 0;
-    unsigned long long* st = a.status + b;
-    if (b == 0) {
-      st_release(st, ST_PRE | (unsigned long long)U);
-    } else {
-      st_release(st, ST_AGG | (unsigned long long)U);
-      int j = b - 1;
-      while (true) {
-        const unsigned long long v = ld_acquire(a.status + j);
-        if (v & ST_PRE) { prefix += (int64_t)(v & ST_VAL); break; }
-        if (v & ST_AGG) { prefix += (int64_t)(v & ST_VAL); --j; }
-      }
-      st_release(st, ST_PRE | (unsigned long long)(prefix + U));
+    int top = b - 1;
+    while (top >= 0) {
+      const int idx = top - lane;
+      const unsigned long long v = idx >= 0 ? ld_acquire(a.status + idx) : ST_PRE;
+      const unsigned pre = __ballot_sync(0xffffffffu, (v & ST_PRE) != 0);
+      const unsigned pub = __ballot_sync(0xffffffffu, v != 0);
+      const int fp = pre ? __ffs(pre) - 1 : 31;
+      const unsigned need = fp == 31 ? 0xffffffffu : ((2u << fp) - 1u);
+      if ((pub & need) != need) continue;   // a predecessor has not published yet
+      int64_t part = (lane <= fp && idx >= 0) ? (int64_t)(v & ST_VAL) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      prefix += part;
+      if (pre) break;
+      top -= 32;
     }
-    s_prefix = prefix;
-    if (b == a.nb - 1) *a.rank_out = prefix + U;
+    if (lane == 0) {
+      if (b > 0) st_release(a.status + b, ST_PRE | (unsigned long long)(prefix + U));
+      s_prefix = prefix;
+      if (b == a.nb - 1) *a.rank_out = prefix + U;
+    }
   }
   __syncthreads();
   const int64_t P = s_prefix;
@@ -477,12 +645,13 @@ __global__ void __launch_bounds__(B_CT, 1) fast_bucket(BucketArgs a) {
 }
 
 __global__ void derive_entries(const int64_t* __restrict__ row1, const int64_t* __restrict__ col1,
-                               int64_t n, int64_t I1, int64_t J1, int64_t* __restrict__ i1,
+                               int64_t n, FastDiv I1, FastDiv J1, int64_t* __restrict__ i1,
                                int64_t* __restrict__ j1) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    if (i1) i1[e] = (row1[e] - 1) % I1;
-    if (j1) j1[e] = (col1[e] - 1) % J1;
+    const uint64_t r0 = (uint64_t)(row1[e] - 1), c0 = (uint64_t)(col1[e] - 1);
+    i1[e] = (int64_t)(r0 - fdiv(I1, r0) * I1.d);
+    j1[e] = (int64_t)(c0 - fdiv(J1, c0) * J1.d);
   }
 }
 
@@ -503,7 +672,7 @@ bool convert_fast(cudaStream_t st, const int64_t* row1, const int64_t* col1, con
   const int s = kb - lgb;
   const int pbits = std::max(1, key_bits((uint64_t)(n - 1)));
   if (s + pbits > 64) return false;
-  KeyMap m{I1, J1, nrb, s, -1};
+  KeyMap m{make_div(I1), make_div(J1), nrb, s, -1};
   const int lgr = key_bits((uint64_t)(nrb - 1));
   if ((nrb & (nrb - 1)) == 0 && s >= lgr) m.bc_shift = s - lgr;
   const int ntiles = (int)cdiv(n, F_TILE);
@@ -515,54 +684,74 @@ bool convert_fast(cudaStream_t st, const int64_t* row1, const int64_t* col1, con
   DBuf<unsigned> thist((size_t)ntiles * nb, st), toff((size_t)ntiles * nb, st), tot(nb, st),
       tkept(ntiles, st);
   DBuf<int64_t> bstart(nb, st), tkoff(ntiles, st), info(2, st);
-  fast_hist<<<ntiles, F_CT, 0, st>>>(row1, col1, val, n, m, nb, thist.get(), tkept.get());
-  CK_LAUNCH();
-  fast_scan_tiles<<<(nb + 31) / 32, 256, 0, st>>>(thist.get(), ntiles, nb, toff.get(), tot.get());
-  CK_LAUNCH();
-  fast_scan_buckets<<<1, 1024, 0, st>>>(tot.get(), nb, tkept.get(), ntiles, bstart.get(),
-                                        tkoff.get(), info.get());
-  CK_LAUNCH();
-  note_launch(3);
-  int64_t h[2] = {0, 0};
-  CK(cudaMemcpyAsync(h, info.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  const int64_t nk = h[0];
-  if (h[1] > B_CAP) return false;   // a bucket too large for one CTA: general path
-  c.nkept = nk;
-  c.ti.alloc(nk, st);
-  if (nk == 0) { c.rank = 0; return true; }
-  const bool zeros = nk < n;
-  if (zeros) {
-    c.i1.alloc(nk, st);
-    c.j1.alloc(nk, st);
-    c.values.alloc(nk, st);
-  } else {
-    c.lazy = true;   // entries derivable from the input: materialised on demand
-    c.src_row = row1;
-    c.src_col = col1;
-    c.src_val = val;
-    c.I1 = I1;
-    c.J1 = J1;
+  DBuf<int> zflag(1, st);
+  // first attempt assumes no explicit zeros (the common case: one read of
+  // the values fewer); fast_scatter verifies and a zero triggers one rerun
+  for (int zero_aware = 0; zero_aware < 2; ++zero_aware) {
+    fast_hist<<<ntiles, F_CT, 0, st>>>(row1, col1, val, n, m, nb, zero_aware != 0, thist.get(),
+                                       tkept.get());
+    CK_LAUNCH();
+    fast_scan_tiles<<<(nb + 31) / 32, 1024, 0, st>>>(thist.get(), ntiles, nb, toff.get(),
+                                                     tot.get());
+    CK_LAUNCH();
+    fast_scan_buckets<<<1, 1024, 0, st>>>(tot.get(), nb, tkept.get(), ntiles, bstart.get(),
+                                          tkoff.get(), info.get());
+    CK_LAUNCH();
+    note_launch(3);
+    int64_t h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, info.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int64_t nk = h[0];
+    if (h[1] > B_CAP) return false;   // a bucket too large for one CTA: general path
+    c.nkept = nk;
+    c.ti.alloc(nk, st);
+    if (nk == 0) { c.rank = 0; return true; }
+    const bool zeros = nk < n;
+    c.lazy = false;
+    c.i1.reset();
+    c.j1.reset();
+    c.values.reset();
+    if (zeros) {
+      c.i1.alloc(nk, st);
+      c.j1.alloc(nk, st);
+      c.values.alloc(nk, st);
+    } else {
+      c.lazy = true;   // entries derivable from the input: materialised on demand
+      c.src_row = row1;
+      c.src_col = col1;
+      c.src_val = val;
+      c.I1 = I1;
+      c.J1 = J1;
+    }
+    DBuf<uint64_t> items(nk, st);
+    CK(cudaMemsetAsync(zflag.get(), 0, sizeof(int), st));
+    ScatterArgs sa{row1, col1, val, n, m, nb, pbits, thist.get(), toff.get(), bstart.get(),
+                   tkoff.get(), zeros, zflag.get(), items.get(), c.i1.get(), c.j1.get(),
+                   c.values.get()};
+    fast_scatter<<<ntiles, F_CT, K3_SMEM, st>>>(sa);
+    CK_LAUNCH();
+    c.uniq.alloc(nk, st);   // capacity: the block count is known after K4
+    DBuf<unsigned> ticket(1, st);
+    DBuf<unsigned long long> status(nb, st);
+    DBuf<int64_t> rank(1, st);
+    CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), st));
+    CK(cudaMemsetAsync(status.get(), 0, sizeof(unsigned long long) * nb, st));
+    // group sort when the low key splits into a block-column part of at
+    // most 11 bits above the block-row bits (nrb a power of two)
+    int gbits = 0;
+    if ((nrb & (nrb - 1)) == 0 && s > lgr && s - lgr <= 11) gbits = s - lgr;
+    BucketArgs ba{items.get(), tot.get(), bstart.get(), nb, s, pbits, gbits, ticket.get(),
+                  status.get(), c.uniq.get(), c.ti.get(), rank.get()};
+    fast_bucket<<<nb, B_CT, K4_SMEM, st>>>(ba);
+    CK_LAUNCH();
+    note_launch(2);
+    int zf = 0;
+    CK(cudaMemcpyAsync(&c.rank, rank.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&zf, zflag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!zf) return true;
   }
-  DBuf<uint64_t> items(nk, st);
-  ScatterArgs sa{row1, col1, val, n, m, nb, pbits, thist.get(), toff.get(), bstart.get(),
-                 tkoff.get(), zeros, items.get(), c.i1.get(), c.j1.get(), c.values.get()};
-  fast_scatter<<<ntiles, F_CT, K3_SMEM, st>>>(sa);
-  CK_LAUNCH();
-  c.uniq.alloc(nk, st);   // capacity: the block count is known after K4
-  DBuf<unsigned> ticket(1, st);
-  DBuf<unsigned long long> status(nb, st);
-  DBuf<int64_t> rank(1, st);
-  CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), st));
-  CK(cudaMemsetAsync(status.get(), 0, sizeof(unsigned long long) * nb, st));
-  BucketArgs ba{items.get(), tot.get(), bstart.get(), nb, s, pbits, ticket.get(), status.get(),
-                c.uniq.get(), c.ti.get(), rank.get()};
-  fast_bucket<<<nb, B_CT, K4_SMEM, st>>>(ba);
-  CK_LAUNCH();
-  note_launch(2);
-  CK(cudaMemcpyAsync(&c.rank, rank.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  return true;
+  throw std::runtime_error("convert_fast: zero-aware pass still saw unaccounted zeros");
 }
 
 void ensure_entries(cudaStream_t st, ConvLocal& c) {
@@ -573,8 +762,8 @@ void ensure_entries(cudaStream_t st, ConvLocal& c) {
   c.values.alloc(n, st);
   if (n > 0) {
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 148 * 16));
-    derive_entries<<<grid, 256, 0, st>>>(c.src_row, c.src_col, n, c.I1, c.J1, c.i1.get(),
-                                         c.j1.get());
+    derive_entries<<<grid, 256, 0, st>>>(c.src_row, c.src_col, n, make_div(c.I1),
+                                         make_div(c.J1), c.i1.get(), c.j1.get());
     CK_LAUNCH();
     note_launch();
     CK(cudaMemcpyAsync(c.values.get(), c.src_val, sizeof(double) * n, cudaMemcpyDeviceToDevice,
