@@ -85,6 +85,12 @@ struct SvdOut {
 // while the floor sits >= 100x below delta.  0: full convergence.
 void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ldm, SvdOut& out,
               double trunc_rel = 0.0);
+// One-CTA variants for matrices that fit shared memory (small.cu); false:
+// not applicable (the blocked paths above take it).
+bool small_qr(cudaStream_t st, int64_t m, int64_t n, const double* A, int64_t lda, double* Q,
+              int64_t ldq, double* R, int64_t ldr);
+bool small_svd(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ldm, SvdOut& out,
+               double trunc_rel);
 
 }  // namespace mpob
 

@@ -660,6 +660,7 @@ static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A
 
 void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda, double* Q,
                     int64_t ldq, double* R, int64_t ldr) {
+  if (small_qr(st, m, n, A, lda, Q, ldq, R, ldr)) return;   // one CTA (small.cu)
   householder_qr_impl(st, m, n, A, lda, Q, ldq, R, ldr, nullptr);
 }
 

@@ -1113,6 +1113,7 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   const int64_t k = std::min(m, n);
   out.k = k;
   if (k <= 0) return;
+  if (small_svd(st, m, n, M, ldm, out, trunc_rel)) return;   // one CTA, converged on chip (small.cu)
   // 32-column blocks for large k, 16-column blocks for small k (the inner
   // Jacobi latency dominates small problems)
   static const int64_t jb_split =

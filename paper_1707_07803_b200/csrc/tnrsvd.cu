@@ -120,6 +120,8 @@ namespace {
 // mpo.py:297-304, evaluated on the host from the device singular values
 int64_t truncation_rank(const std::vector<double>& s, double delta, double rel_tol) {
   const int64_t n = (int64_t)s.size();
+  for (double v : s)
+    if (std::isnan(v)) throw std::runtime_error("svd: Jacobi iteration did not converge");
   if (rel_tol == 0.0) {
     int64_t nz = 0;
     for (double v : s) nz += (v != 0.0);
