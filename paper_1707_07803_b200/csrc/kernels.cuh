@@ -91,6 +91,11 @@ bool small_qr(cudaStream_t st, int64_t m, int64_t n, const double* A, int64_t ld
               int64_t ldq, double* R, int64_t ldr);
 bool small_svd(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ldm, SvdOut& out,
                double trunc_rel);
+// Inverse of a k x k upper-triangular matrix, and the certified lower
+// bound 1 / ||U^{-1}||_F <= sigma_min(U) (rankcert.cu).
+void tri_inv_upper(cudaStream_t st, int64_t k, const double* U, int64_t ldu, double* Out);
+double min_sv_lower_bound(cudaStream_t st, int64_t k, const double* U, int64_t ldu,
+                          double target);
 
 }  // namespace mpob
 

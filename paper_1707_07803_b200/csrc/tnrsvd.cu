@@ -170,11 +170,46 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
   const size_t d = cores.size();
   if (d == 1) return;
   const double delta = tol * device_norm(st, cores.back()) / std::sqrt((double)(d - 1));
+  // rank certificate (rankcert.cu): skip the SVD of a wide unfolding whose
+  // smallest singular value provably exceeds delta (nothing to discard)
+  static const bool cert_on =
+      std::getenv("MPO_B200_RANKCERT") ? std::atoi(std::getenv("MPO_B200_RANKCERT")) != 0 : true;
+  static const int64_t cert_min =
+      std::getenv("MPO_B200_RANKCERT_MIN") ? std::atoll(std::getenv("MPO_B200_RANKCERT_MIN")) : 256;
+  constexpr double cert_margin = 4.0;
   for (size_t k = d - 1; k >= 1; --k) {
     Core& c = cores[k];
     const int64_t R = c.R, N = c.I * c.J * c.S;
     Core& pv = cores[k - 1];
     const int64_t Mp = pv.R * pv.I * pv.J;
+    if (cert_on && R >= cert_min && R <= N) {
+      // LQ: M^T = Q' R'  (N x R, R x R)
+      DBuf<double> At((size_t)N * R, st), Qt((size_t)N * R, st), Rt((size_t)R * R, st);
+      {
+        Trace tr(st, "lq", R, N);
+        int64_t dims[2] = {R, N};
+        int pr[2] = {1, 0};
+        permute(st, c.p(), At.get(), 2, dims, pr);
+        householder_qr(st, N, R, At.get(), N, Qt.get(), N, Rt.get(), R);
+      }
+      double lb;
+      {
+        Trace tr(st, "rank_cert", R, R);
+        lb = min_sv_lower_bound(st, R, Rt.get(), R, cert_margin * delta);
+      }
+      if (lb > cert_margin * delta) {
+        // M = R'^T Q'^T: core k <- Q'^T (orthonormal rows), core k-1 absorbs R'^T
+        Core nc = make_core(st, R, c.I, c.J, c.S);
+        int64_t dims[2] = {N, R};
+        int pr[2] = {1, 0};
+        permute(st, Qt.get(), nc.p(), 2, dims, pr);
+        Core np_ = make_core(st, pv.R, pv.I, pv.J, R);
+        dgemm(st, false, true, Mp, R, R, 1.0, pv.p(), Mp, Rt.get(), R, 0.0, np_.p(), Mp);
+        cores[k] = std::move(nc);
+        cores[k - 1] = std::move(np_);
+        continue;
+      }
+    }
     SvdOut o;
     {
       Trace tr(st, "svd", R, N);
