@@ -774,6 +774,33 @@ __global__ void sort_desc_kernel(const double* vals, int n, int npow2, double* s
   for (int i = threadIdx.x; i < n; i += blockDim.x) { sorted[i] = v[i]; perm[i] = ix[i]; }
 }
 
+// descending sort by rank counting (k > 8192, beyond one CTA's shared
+// memory): rank_i = #{j : v_j > v_i or (v_j == v_i and j < i)}; one thread
+// per element, the values streamed through shared-memory tiles
+__global__ void __launch_bounds__(256) rank_sort_kernel(const double* __restrict__ vals, int n,
+                                                        double* __restrict__ sorted,
+                                                        int* __restrict__ perm) {
+  __shared__ double tile[2048];
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  const double vi = i < n ? vals[i] : 0.0;
+  int rank = 0;
+  for (int t0 = 0; t0 < n; t0 += 2048) {
+    const int m = min(2048, n - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < m; e += 256) tile[e] = vals[t0 + e];
+    __syncthreads();
+    if (i < n)
+      for (int e = 0; e < m; ++e) {
+        const double vj = tile[e];
+        rank += (vj > vi) || (vj == vi && t0 + e < i);
+      }
+  }
+  if (i < n) {
+    sorted[rank] = vi;
+    perm[rank] = i;
+  }
+}
+
 // B[:, j] = A[0:rows, perm[j]]
 __global__ void gather_cols_kernel(const double* A, int64_t lda, int64_t rows, const int* perm,
                                    int64_t ncols, double* B, int64_t ldb) {
@@ -1181,13 +1208,21 @@ void svd_thin(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t ld
   CK_LAUNCH();
   int np2 = 1;
   while (np2 < kp) np2 <<= 1;
-  if (np2 > 8192) throw ValueError("svd: k > 8192 not supported by the single-CTA sort");
   DBuf<int> perm(kp, st);
   out.s.alloc(k, st);
-  size_t ssmem = (size_t)np2 * (sizeof(double) + sizeof(int));
-  if (ssmem > 48 * 1024)
-    CK(cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
-  sort_desc_kernel<<<1, 1024, ssmem, st>>>(norms.get(), (int)kp, np2, norms.get(), perm.get());
+  if (np2 <= 8192) {
+    size_t ssmem = (size_t)np2 * (sizeof(double) + sizeof(int));
+    if (ssmem > 48 * 1024)
+      CK(cudaFuncSetAttribute(sort_desc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+    sort_desc_kernel<<<1, 1024, ssmem, st>>>(norms.get(), (int)kp, np2, norms.get(), perm.get());
+  } else {
+    DBuf<double> sorted(kp, st);
+    rank_sort_kernel<<<(int)cdiv(kp, 256), 256, 0, st>>>(norms.get(), (int)kp, sorted.get(),
+                                                        perm.get());
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(norms.get(), sorted.get(), sizeof(double) * kp, cudaMemcpyDeviceToDevice,
+                       st));
+  }
   CK_LAUNCH();
   CK(cudaMemcpyAsync(out.s.get(), norms.get(), sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
   note_launch(2);

@@ -210,6 +210,29 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         continue;
       }
     }
+    if (cert_on && N >= cert_min && R > N) {
+      // tall unfolding: the rank drops to N at most; if sigma_min(M) > delta
+      // it is exactly N and M = M * I_N -- core k <- identity (orthonormal
+      // rows), core k-1 absorbs M (no factorisation of M needed beyond the
+      // certificate's R factor)
+      DBuf<double> Mc((size_t)R * N, st), Qm((size_t)R * N, st), Rm((size_t)N * N, st);
+      copy_matrix(st, R, N, c.p(), R, Mc.get(), R);
+      double lb;
+      {
+        Trace tr(st, "rank_cert_tall", R, N);
+        householder_qr(st, R, N, Mc.get(), R, Qm.get(), R, Rm.get(), N);
+        lb = min_sv_lower_bound(st, N, Rm.get(), N, cert_margin * delta);
+      }
+      if (lb > cert_margin * delta) {
+        Core nc = make_core(st, N, c.I, c.J, c.S);
+        set_identity(st, N, N, nc.p(), N);
+        Core np_ = make_core(st, pv.R, pv.I, pv.J, N);
+        dgemm(st, false, false, Mp, N, R, 1.0, pv.p(), Mp, c.p(), R, 0.0, np_.p(), Mp);
+        cores[k] = std::move(nc);
+        cores[k - 1] = std::move(np_);
+        continue;
+      }
+    }
     SvdOut o;
     {
       Trace tr(st, "svd", R, N);
