@@ -27,8 +27,8 @@ for i, m in data.items():
     a[2] += m.get("dram__bytes_read.sum", 0) / 1e6
     a[3] += m.get("dram__bytes_write.sum", 0) / 1e6
 tot = sum(a[1] for a in agg.values())
-print(f"{'kernel':42s} {'n':>4s} {'us/launch':>10s} {'share':>6s} {'MB rd':>8s} {'MB wr':>8s} {'GB/s':>7s}")
+print(f"{'kernel':42s} {'n':>4s} {'us/launch':>10s} {'share':>6s} {'MB rd':>8s} {'MB wr':>8s} {'TB/s':>7s}")
 for k, (n, us, rd, wr) in agg.items():
     print(f"{k:42s} {n:4d} {us / n:10.1f} {us / tot:6.1%} {rd / n:8.1f} {wr / n:8.1f} "
-          f"{(rd + wr) / us * 1e3 / 1e3 if us else 0:7.0f}")
+          f"{(rd + wr) / us if us else 0:7.2f}")
 print(f"total {tot:.1f} us over {sum(a[0] for a in agg.values())} launches")
