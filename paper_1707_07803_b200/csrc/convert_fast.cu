@@ -13,11 +13,19 @@
 //                    the bucket regions                        read row, col, val;
 //                                                              write 8 B / entry
 //   K4 fast_bucket   per bucket (<= 16K entries, taken in bucket order from a
-//                    ticket): stable LSD sort of the low key bits on chip
-//                    (10-bit digits, warp-private counters + ballot multisplit),
-//                    head flags -> local block ids, decoupled look-back over
-//                    the preceding buckets for the global id offset, then
-//                    uniq (coalesced) and ti[position]        read 8 B, write
+//                    ticket), 32 warps: for the square 2^k plans a stable
+//                    counting pass on the block-column bits (ballot
+//                    multisplit, warp-private counters) groups each block
+//                    column's items in fast_scatter (tile) order -- for
+//                    row-sorted input already ordered by block row except
+//                    where two entries of one column met in one tile -- then
+//                    only groups with a key inversion are re-sorted (one
+//                    warp each); other plans and oversize groups take stable
+//                    10-bit LSD passes.  Head flags -> local block ids,
+//                    decoupled look-back over the preceding buckets (the
+//                    whole CTA polls 1024 predecessors per step, relaxed
+//                    loads) for the global id offset, then uniq (coalesced)
+//                    and ti[position]                          read 8 B, write
 //                                                              8 B/block + 8 B
 // Compulsory traffic is 32 B/entry + 8 B/block; this path
 // moves ~64 B/entry + 8 B/block plus the random ti scatter.  Ties between
@@ -31,6 +39,11 @@
 #include "common.cuh"
 #include "convert.cuh"
 #include "kernels.cuh"
+#ifdef MPO_CONV_PROF
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#endif
 
 namespace mpob {
 
@@ -40,23 +53,27 @@ constexpr int F_CT = 512;                 // tile CTAs (K1, K3)
 constexpr int F_IT = 32;
 constexpr int F_TILE = F_CT * F_IT;       // 16384 entries per tile
 constexpr int F_MAXB = 4096;              // buckets
-constexpr int B_CT = 512;                 // bucket CTAs (K4)
+constexpr int B_CT = 1024;                // bucket CTAs (K4), one per SM (measured: the same
+constexpr int B_MINB = 1;                 // as two 512-thread CTAs on half-size buckets)
 constexpr int B_W = B_CT / 32;
-constexpr int B_IT = 32;
+constexpr int B_IT = 16;
 constexpr int B_CAP = B_CT * B_IT;        // 16384 entries per bucket
 constexpr int B_RB = 10;
 constexpr int B_R = 1 << B_RB;            // local digit bins
-constexpr unsigned long long ST_AGG = 1ull << 62, ST_PRE = 2ull << 62,
-                             ST_VAL = (1ull << 62) - 1;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+constexpr unsigned long long ST_AGG = 1ull << 62, ST_PRE = 2ull << 62,
+                             ST_VAL = (1ull << 62) - 1;
+// status words carry their whole payload (flag | value), so the look-back
+// polls with relaxed L2 loads (an acquire load would invalidate L1 on every
+// poll) and publishes with a release store
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
@@ -97,7 +114,7 @@ __global__ void __launch_bounds__(F_CT, 2) fast_hist(const int64_t* __restrict__
                                                   const int64_t* __restrict__ col1,
                                                   const double* __restrict__ val, int64_t n,
                                                   KeyMap m, int nb, bool zero_aware,
-                                                  unsigned* __restrict__ thist,
+                                                  uint16_t* __restrict__ thist,
                                                   unsigned* __restrict__ tkept) {
   // zero_aware = false: every entry counted as kept (fast_scatter checks the
   // values and flags a rerun with zero_aware = true if any is zero)
@@ -141,17 +158,17 @@ __global__ void __launch_bounds__(F_CT, 2) fast_hist(const int64_t* __restrict__
     for (int w = 0; w < F_CT / 32; ++w) t += wsum[w];
     tkept[blockIdx.x] = t;
   }
-  unsigned* out = thist + (int64_t)blockIdx.x * nb;
-  for (int i = threadIdx.x; i < nb; i += F_CT) out[i] = h[i];
+  uint16_t* out = thist + (int64_t)blockIdx.x * nb;
+  for (int i = threadIdx.x; i < nb; i += F_CT) out[i] = (uint16_t)h[i];
 }
 
 // ---------------- K2 -------------------------------------------------------
 // per bucket (lane), 32 warps over contiguous tile segments, 8 loads in
 // flight per lane: tile prefix of the bucket counts (toff, without the
 // bucket start) and the bucket totals
-__global__ void __launch_bounds__(1024) fast_scan_tiles(const unsigned* __restrict__ thist,
+__global__ void __launch_bounds__(1024) fast_scan_tiles(const uint16_t* __restrict__ thist,
                                                         int ntiles, int nb,
-                                                        unsigned* __restrict__ toff,
+                                                        uint16_t* __restrict__ toff,
                                                         unsigned* __restrict__ tot) {
   __shared__ unsigned ssum[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -183,14 +200,14 @@ __global__ void __launch_bounds__(1024) fast_scan_tiles(const unsigned* __restri
       for (int u = 0; u < U; ++u) v[u] = thist[(int64_t)(t + u) * nb + b];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        toff[(int64_t)(t + u) * nb + b] = run;
+        toff[(int64_t)(t + u) * nb + b] = (uint16_t)run;
         run += v[u];
       }
     }
     for (; t < t1; ++t) {
       const int64_t o = (int64_t)t * nb + b;
       const unsigned v = thist[o];
-      toff[o] = run;
+      toff[o] = (uint16_t)run;
       run += v;
     }
     if (warp == 31) tot[b] = run;
@@ -251,8 +268,9 @@ struct ScatterArgs {
   int64_t n;
   KeyMap m;
   int nb, pbits;
-  const unsigned* thist;
-  const unsigned* toff;
+  const uint16_t* thist;   // per tile and bucket: count (< 2^16: a tile holds 16K entries)
+  const uint16_t* toff;    // per tile and bucket: offset inside the bucket (buckets
+                           // above B_CAP < 2^16 entries never reach fast_scatter)
   const int64_t* bstart;
   const int64_t* tkoff;
   bool zeros;          // explicit zeros present: compact, write i1/j1/values
@@ -276,7 +294,7 @@ __global__ void __launch_bounds__(F_CT) fast_scatter(ScatterArgs a) {
   __shared__ unsigned s_total;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = a.nb;
-  const unsigned* hrow = a.thist + (int64_t)blockIdx.x * nb;
+  const uint16_t* hrow = a.thist + (int64_t)blockIdx.x * nb;
   // tile-local bucket offsets: exclusive scan of this tile's histogram row
   {
     constexpr int PER = F_MAXB / F_CT;   // 8 buckets per thread (nb <= 4096)
@@ -364,7 +382,7 @@ __global__ void __launch_bounds__(F_CT) fast_scatter(ScatterArgs a) {
   if (saw_zero) atomicOr(a.zero_found, 1);
   __syncthreads();
   // global start of this tile's run in each bucket (n < 2^31: fits 32 bits)
-  const unsigned* trow = a.toff + (int64_t)blockIdx.x * nb;
+  const uint16_t* trow = a.toff + (int64_t)blockIdx.x * nb;
   for (int b = tid; b < nb; b += F_CT) cur[b] = (unsigned)(a.bstart[b] + trow[b]) - loff[b];
   __syncthreads();
   const unsigned cnt = s_total;
@@ -372,13 +390,30 @@ __global__ void __launch_bounds__(F_CT) fast_scatter(ScatterArgs a) {
 }
 
 // ---------------- K4 -------------------------------------------------------
+#ifdef MPO_CONV_PROF
+// clock64 per phase of fast_bucket, summed over buckets (variant builds only:
+// tools/build_variant.sh k4prof convert_fast.cu -DMPO_CONV_PROF)
+__device__ unsigned long long g_k4prof[10];
+#define K4MARK(i)                                                   \
+  do {                                                              \
+    __syncthreads();                                                \
+    if (threadIdx.x == 0) {                                         \
+      const long long t_ = clock64();                               \
+      atomicAdd(&g_k4prof[i], (unsigned long long)(t_ - t_prev));   \
+      t_prev = t_;                                                  \
+    }                                                               \
+  } while (0)
+#else
+#define K4MARK(i) do {} while (0)
+#endif
 struct BucketArgs {
   const uint64_t* items;
   const unsigned* tot;
   const int64_t* bstart;
   int nb, s, pbits;
-  int gbits;   // > 0: group sort (the low key's top gbits select a group, the
-               // rest orders items inside it); 0: LSD passes over all s bits
+  int gbits;   // > 0: group sort (the low key's top gbits select a group --
+               // for the square 2^k plans the block column inside the bucket);
+               // 0: LSD passes over all s bits
   unsigned* ticket;
   unsigned long long* status;
   int64_t* uniq;
@@ -387,98 +422,179 @@ struct BucketArgs {
 };
 
 constexpr size_t K4_SMEM = (size_t)B_CAP * sizeof(uint64_t) +
-                           (size_t)B_W * B_R * sizeof(uint16_t) + (size_t)B_R * sizeof(unsigned);
+                           (size_t)B_W * B_R * sizeof(uint16_t) +
+                           (size_t)(B_R + 1) * sizeof(unsigned) + (size_t)B_R;
 
-__global__ void __launch_bounds__(B_CT, 1) fast_bucket(BucketArgs a) {
+// Stable counting pass over the bucket's items x (warp-contiguous: item
+// j = warp * wlen + it * 32 + lane for it < reff; slots j >= cnt hold ~0 and
+// so sort last) on the digit (x >> shift) & (2^nbits - 1), nbits <= B_RB:
+// ranks from warp-private digit counters and a ballot multisplit (lanes with
+// equal digits: AND of one ballot per digit bit), A receives the items in
+// digit order with ties in their incoming order, x is reloaded from A, and
+// dst0[0 .. 2^nbits] holds the digit starts (dst0[2^nbits] = total).
+__device__ void stable_pass(uint64_t (&x)[B_IT], int reff, int shift, int nbits, uint64_t* A,
+                            uint16_t* wh, unsigned* dst0, unsigned* wtot) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nbin = 1 << nbits;
+  const unsigned dmask = (unsigned)nbin - 1u;
+  const int wlen = reff * 32;
+  for (int i = tid; i < B_W * nbin; i += B_CT) wh[i] = 0;
+  __syncthreads();
+  unsigned rk[B_IT / 2];
+#pragma unroll
+  for (int it = 0; it < B_IT; ++it) {
+    if (it < reff) {
+      const unsigned d = (unsigned)(x[it] >> shift) & dmask;
+#ifdef K4_MATCH
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+#else
+      unsigned peers = 0xffffffffu;
+      for (int k = 0; k < nbits; ++k) {
+        const bool bit = (d >> k) & 1u;
+        const unsigned bt = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bt : ~bt;
+      }
+#endif
+      const unsigned run = wh[warp * nbin + d];
+      const unsigned r = run + __popc(peers & lanemask_lt());
+      if (it & 1) rk[it >> 1] |= r << 16; else rk[it >> 1] = r;
+      __syncwarp();
+      if ((__ffs(peers) - 1) == lane) wh[warp * nbin + d] = (uint16_t)(run + __popc(peers));
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // per digit: exclusive prefix over the warps (in place) and the digit total
+  for (int d = tid; d < nbin; d += B_CT) {
+    unsigned acc = 0;
+    for (int w = 0; w < B_W; ++w) {
+      const unsigned v = wh[w * nbin + d];
+      wh[w * nbin + d] = (uint16_t)acc;
+      acc += v;
+    }
+    dst0[d] = acc;
+  }
+  __syncthreads();
+  // exclusive scan of the nbin <= B_R digit totals, PD consecutive per thread
+  {
+    constexpr int PD = (B_R + B_CT - 1) / B_CT;
+    unsigned v[PD], sum = 0;
+#pragma unroll
+    for (int q = 0; q < PD; ++q) {
+      const int d = tid * PD + q;
+      v[q] = d < nbin ? dst0[d] : 0u;
+      sum += v[q];
+    }
+    unsigned inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wtot[warp] = inc;
+    __syncthreads();
+    unsigned run = inc - sum;
+    for (int w = 0; w < warp; ++w) run += wtot[w];
+#pragma unroll
+    for (int q = 0; q < PD; ++q) {
+      const int d = tid * PD + q;
+      if (d < nbin) dst0[d] = run;
+      run += v[q];
+    }
+    if (tid == B_CT - 1) dst0[nbin] = run;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < B_IT; ++it) {
+    if (it < reff) {
+      const unsigned d = (unsigned)(x[it] >> shift) & dmask;
+      const unsigned r = (it & 1) ? (rk[it >> 1] >> 16) : (rk[it >> 1] & 0xffffu);
+      A[dst0[d] + wh[warp * nbin + d] + r] = x[it];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < B_IT; ++it)
+    if (it < reff) x[it] = A[warp * wlen + it * 32 + lane];
+}
+
+__global__ void __launch_bounds__(B_CT, B_MINB) fast_bucket(BucketArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   uint64_t* A = reinterpret_cast<uint64_t*>(sm);
   uint16_t* wh = reinterpret_cast<uint16_t*>(sm + (size_t)B_CAP * sizeof(uint64_t));
   unsigned* dst0 = reinterpret_cast<unsigned*>(wh + B_W * B_R);
+  unsigned char* gflag = reinterpret_cast<unsigned char*>(dst0 + B_R + 1);
   __shared__ unsigned s_b, wtot[B_W];
-  __shared__ int64_t s_prefix;
+  __shared__ int s_big, s_fpw[B_W];
+  __shared__ int64_t s_partw[B_W];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // buckets are taken in ticket order: every predecessor a look-back waits
+  // for is resident or done
   if (tid == 0) s_b = atomicAdd(a.ticket, 1u);
   __syncthreads();
   const int b = (int)s_b;
   const int cnt = (int)a.tot[b];
   const int64_t start = a.bstart[b];
+#ifdef MPO_CONV_PROF
+  long long t_prev = clock64();
+#endif
   // warp-contiguous layout over the rounds actually needed
   const int reff = (cnt + B_CT - 1) / B_CT;          // rounds per warp
   const int wlen = reff * 32;                        // items per warp
+  // x = ~0: padding (no valid item is ~0: the host keeps s + pbits < 64)
   uint64_t x[B_IT];
 #pragma unroll
   for (int it = 0; it < B_IT; ++it) {
     const int j = warp * wlen + it * 32 + lane;
     x[it] = (it < reff && j < cnt) ? a.items[start + j] : ~0ull;
   }
-  // Group sort: one counting pass on the low key's top gbits (for the
-  // square 2^k plans: the block column inside the bucket) puts every
-  // block column's items together; each group (~16 items on average) is
-  // then ordered by one thread (insertion sort on the whole item, i.e. by
-  // block row, then position).  Buckets whose largest group exceeds
-  // GMAX take the LSD passes instead.
+  const uint64_t* Aw = A + warp * wlen + lane;   // item it of this lane at Aw[it * 32]
+  const bool lead = warp == 0 && lane == 0;      // item 0 of the bucket
+  K4MARK(0);
+  // Group sort: a stable counting pass on the low key's top gbits (for the
+  // square 2^k plans: the block column inside the bucket) puts every block
+  // column's items together in their fast_scatter order -- tile order, so
+  // for row-sorted input already ordered by block row except for entries
+  // of one column that met in the same tile.  Groups with a key inversion
+  // are re-sorted by one warp each (rank sort on the whole item, items are
+  // distinct: they carry their position); a flagged group above GMAX items
+  // sends the bucket to the LSD passes.
   constexpr int GMAX = 64;
-  __shared__ int s_general;
-  bool sorted_in_A = false;
+  bool sorted = false;
   if (a.gbits > 0) {
-    unsigned* gh = reinterpret_cast<unsigned*>(wh);          // counts, then offsets
-    unsigned* gc = gh + (1 << a.gbits);                      // cursors
     const int G = 1 << a.gbits;
     const int gshift = a.pbits + a.s - a.gbits;
-    for (int g = tid; g < G; g += B_CT) { gh[g] = 0; gc[g] = 0; }
-    if (tid == 0) s_general = 0;
+    stable_pass(x, reff, gshift, a.gbits, A, wh, dst0, wtot);
+    K4MARK(1);
+    for (int g = tid; g < G; g += B_CT) gflag[g] = 0;
+    if (tid == 0) s_big = 0;
     __syncthreads();
+    bool inv = false;
 #pragma unroll
-    for (int it = 0; it < B_IT; ++it)
-      if (it < reff && warp * wlen + it * 32 + lane < cnt)
-        atomicAdd(&gh[(unsigned)(x[it] >> gshift) & (G - 1)], 1u);
-    __syncthreads();
-    // exclusive scan of the G (<= 2048) group counts, 4 per thread
-    {
-      unsigned v[4], sum = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int g = tid * 4 + q;
-        v[q] = g < G ? gh[g] : 0u;
-        sum += v[q];
-        if (v[q] > GMAX) s_general = 1;
-      }
-      unsigned inc = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      if (lane == 31) wtot[warp] = inc;
-      __syncthreads();
-      unsigned run = inc - sum;
-      for (int w = 0; w < warp; ++w) run += wtot[w];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int g = tid * 4 + q;
-        if (g < G) gh[g] = run;
-        run += v[q];
+    for (int it = 0; it < B_IT; ++it) {
+      if (it < reff && x[it] != ~0ull && !(it == 0 && lead)) {
+        const uint64_t p = Aw[it * 32 - 1];
+        if ((p >> gshift) == (x[it] >> gshift) && (p >> a.pbits) > (x[it] >> a.pbits)) {
+          gflag[(unsigned)(x[it] >> gshift)] = 1;
+          inv = true;
+        }
       }
     }
-    __syncthreads();
-    if (!s_general) {
-#pragma unroll
-      for (int it = 0; it < B_IT; ++it)
-        if (it < reff && warp * wlen + it * 32 + lane < cnt) {
-          const unsigned g = (unsigned)(x[it] >> gshift) & (G - 1);
-          A[gh[g] + atomicAdd(&gc[g], 1u)] = x[it];
-        }
-      __syncthreads();
-      // one warp per group, rank sort: every lane counts the group's
-      // smaller items through independent shuffles (items are distinct:
-      // they carry their position) and stores its item at that rank
+    const int any_inv = __syncthreads_or(inv);
+    K4MARK(2);
+    if (any_inv) {
       for (int g = warp; g < G; g += B_W) {
-        const unsigned lo = gh[g], n_g = gc[g];
-        if (n_g <= 1) continue;
+        if (!gflag[g]) continue;
+        const unsigned lo = dst0[g], n_g = min(dst0[g + 1], (unsigned)cnt) - lo;
+        if (n_g > GMAX) {
+          if (lane == 0) s_big = 1;
+          continue;
+        }
         if (n_g <= 32) {
           const uint64_t v = lane < (int)n_g ? A[lo + lane] : ~0ull;
           unsigned r = 0;
           for (int i = 0; i < (int)n_g; ++i) r += __shfl_sync(0xffffffffu, v, i) < v;
+          __syncwarp();
           if (lane < (int)n_g) A[lo + r] = v;
         } else {
           const uint64_t v0 = A[lo + lane];
@@ -490,158 +606,94 @@ __global__ void __launch_bounds__(B_CT, 1) fast_bucket(BucketArgs a) {
             r0 += o < v0;
             r1 += o < v1;
           }
+          __syncwarp();
           A[lo + r0] = v0;
           if (lane + 32 < (int)n_g) A[lo + r1] = v1;
         }
       }
       __syncthreads();
+      if (!s_big) {
 #pragma unroll
-      for (int it = 0; it < B_IT; ++it)
-        if (it < reff) x[it] = A[warp * wlen + it * 32 + lane];
-      sorted_in_A = true;
+        for (int it = 0; it < B_IT; ++it)
+          if (it < reff) x[it] = A[warp * wlen + it * 32 + lane];
+      }
     }
+    sorted = !s_big;
     __syncthreads();
+    K4MARK(3);
   }
-  const int npass = sorted_in_A ? 0 : (a.s + B_RB - 1) / B_RB;
-  for (int pass = 0; pass < npass; ++pass) {
-    const int shift = a.pbits + pass * B_RB;
-    for (int i = tid; i < B_W * B_R; i += B_CT) wh[i] = 0;
-    __syncthreads();
-    unsigned rk[B_IT / 2];
-#pragma unroll
-    for (int it = 0; it < B_IT; ++it) {
-      if (it < reff) {
-        const unsigned d = (unsigned)(x[it] >> shift) & (B_R - 1);
-        // lanes holding the same digit: AND of one ballot per digit bit
-        // (cheaper than __match_any_sync, whose latency stalled this loop)
-        unsigned peers = 0xffffffffu;
-#pragma unroll
-        for (int k = 0; k < B_RB; ++k) {
-          const bool bit = (d >> k) & 1u;
-          const unsigned bt = __ballot_sync(0xffffffffu, bit);
-          peers &= bit ? bt : ~bt;
-        }
-        const unsigned run = wh[warp * B_R + d];
-        const unsigned r = run + __popc(peers & lanemask_lt());
-        if (it & 1) rk[it >> 1] |= r << 16; else rk[it >> 1] = r;
-        __syncwarp();
-        if ((__ffs(peers) - 1) == lane) wh[warp * B_R + d] = (uint16_t)(run + __popc(peers));
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    // per digit: exclusive prefix over warps (in place), digit totals
-    for (int d = tid; d < B_R; d += B_CT) {
-      unsigned acc = 0;
-      for (int w = 0; w < B_W; ++w) {
-        const unsigned v = wh[w * B_R + d];
-        wh[w * B_R + d] = (uint16_t)acc;
-        acc += v;
-      }
-      dst0[d] = acc;
-    }
-    __syncthreads();
-    // exclusive scan of the digit totals (B_R = 1024 over 512 threads: 2 each)
-    {
-      const unsigned v0 = dst0[2 * tid], v1 = dst0[2 * tid + 1];
-      unsigned inc = v0 + v1;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      if (lane == 31) wtot[warp] = inc;
-      __syncthreads();
-      unsigned wb = 0;
-      for (int w = 0; w < warp; ++w) wb += wtot[w];
-      const unsigned ex = wb + inc - v0 - v1;
-      __syncthreads();
-      dst0[2 * tid] = ex;
-      dst0[2 * tid + 1] = ex + v0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < B_IT; ++it) {
-      if (it < reff) {
-        const unsigned d = (unsigned)(x[it] >> shift) & (B_R - 1);
-        const unsigned r = (it & 1) ? (rk[it >> 1] >> 16) : (rk[it >> 1] & 0xffffu);
-        A[dst0[d] + wh[warp * B_R + d] + r] = x[it];
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < B_IT; ++it)
-      if (it < reff) x[it] = A[warp * wlen + it * 32 + lane];
-    __syncthreads();
-  }
-  if (npass == 0 && !sorted_in_A) {   // one key per bucket: publish for the neighbour reads
+  const int npass = sorted ? 0 : (a.s + B_RB - 1) / B_RB;
+  for (int pass = 0; pass < npass; ++pass)
+    stable_pass(x, reff, a.pbits + pass * B_RB, min(B_RB, a.s - pass * B_RB), A, wh, dst0, wtot);
+  if (!sorted && npass == 0) {   // one key per bucket: publish for the neighbour reads
 #pragma unroll
     for (int it = 0; it < B_IT; ++it)
       if (it < reff) A[warp * wlen + it * 32 + lane] = x[it];
-    __syncthreads();
   }
-  // head flags in sorted order -> local ids
-  unsigned ball[B_IT];
-  unsigned mine = 0;
+  __syncthreads();
+  K4MARK(4);
+  // head flags in sorted order -> local ids (flags kept as a bit mask)
+  unsigned mine = 0, hbits = 0;
 #pragma unroll
   for (int it = 0; it < B_IT; ++it) {
-    ball[it] = 0;
     if (it < reff) {
-      const int j = warp * wlen + it * 32 + lane;
-      const uint64_t lo = x[it] >> a.pbits;
-      const bool head = j < cnt && (j == 0 || (A[j - 1] >> a.pbits) != lo);
-      ball[it] = __ballot_sync(0xffffffffu, head);
-      mine += __popc(ball[it]);
+      const bool head = x[it] != ~0ull &&
+                        ((it == 0 && lead) || (Aw[it * 32 - 1] >> a.pbits) != (x[it] >> a.pbits));
+      hbits |= (unsigned)head << it;
+      mine += __popc(__ballot_sync(0xffffffffu, head));
     }
   }
   if (lane == 0) wtot[warp] = mine;
   __syncthreads();
   unsigned wbase = 0, U = 0;
   for (int w = 0; w < B_W; ++w) { const unsigned v = wtot[w]; wbase += w < warp ? v : 0; U += v; }
-  // decoupled look-back over the preceding buckets (ticket order), one warp
-  // reading 32 predecessors' status words per step
-  if (warp == 0) {
-    if (lane == 0) st_release(a.status + b, (b == 0 ? ST_PRE : ST_AGG) | (unsigned long long)U);
-    int64_t prefix = 0;
-    int top = b - 1;
-    while (top >= 0) {
-      const int idx = top - lane;
-      const unsigned long long v = idx >= 0 ? ld_acquire(a.status + idx) : ST_PRE;
-      const unsigned pre = __ballot_sync(0xffffffffu, (v & ST_PRE) != 0);
-      const unsigned pub = __ballot_sync(0xffffffffu, v != 0);
-      const int fp = pre ? __ffs(pre) - 1 : 31;
-      const unsigned need = fp == 31 ? 0xffffffffu : ((2u << fp) - 1u);
-      if ((pub & need) != need) continue;   // a predecessor has not published yet
-      int64_t part = (lane <= fp && idx >= 0) ? (int64_t)(v & ST_VAL) : 0;
+  K4MARK(5);
+  // decoupled look-back over the preceding buckets (ticket order): the whole
+  // CTA reads B_CT predecessors' status words per step -- the nearest
+  // inclusive prefix is usually among the ~2 x 148 buckets in flight
+  if (tid == 0) st_release(a.status + b, (b == 0 ? ST_PRE : ST_AGG) | (unsigned long long)U);
+  int64_t prefix = 0;
+  for (int top = b - 1; top >= 0;) {
+    const int idx = top - tid;
+    const unsigned long long v = idx >= 0 ? ld_relaxed(a.status + idx) : ST_PRE;
+    const unsigned pre = __ballot_sync(0xffffffffu, (v & ST_PRE) != 0);
+    if (lane == 0) s_fpw[warp] = pre ? warp * 32 + __ffs(pre) - 1 : B_CT;
+    __syncthreads();
+    int fp = B_CT;   // nearest predecessor with an inclusive prefix (B_CT: none in this step)
+    for (int w = 0; w < B_W; ++w) fp = min(fp, s_fpw[w]);
+    int64_t part = (tid <= fp && idx >= 0) ? (int64_t)(v & ST_VAL) : 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      prefix += part;
-      if (pre) break;
-      top -= 32;
-    }
-    if (lane == 0) {
-      if (b > 0) st_release(a.status + b, ST_PRE | (unsigned long long)(prefix + U));
-      s_prefix = prefix;
-      if (b == a.nb - 1) *a.rank_out = prefix + U;
-    }
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) s_partw[warp] = part;
+    // a predecessor up to fp has not published yet: read again
+    if (__syncthreads_or(tid <= fp && v == 0)) continue;
+    for (int w = 0; w < B_W; ++w) prefix += s_partw[w];
+    __syncthreads();
+    if (fp < B_CT) break;
+    top -= B_CT;
   }
-  __syncthreads();
-  const int64_t P = s_prefix;
+  if (tid == 0) {
+    if (b > 0) st_release(a.status + b, ST_PRE | (unsigned long long)(prefix + U));
+    if (b == a.nb - 1) *a.rank_out = prefix + U;
+  }
+  K4MARK(6);
+  const int64_t P = prefix;
   const uint64_t pmask = (1ull << a.pbits) - 1;
   unsigned run = wbase;
 #pragma unroll
   for (int it = 0; it < B_IT; ++it) {
     if (it < reff) {
-      const int j = warp * wlen + it * 32 + lane;
-      if (j < cnt) {
-        const bool head = (ball[it] >> lane) & 1u;
-        const int64_t id = P + run + __popc(ball[it] & lanemask_lt()) + (head ? 1 : 0) - 1;
+      const bool head = (hbits >> it) & 1u;
+      const unsigned ball = __ballot_sync(0xffffffffu, head);
+      if (x[it] != ~0ull) {
+        const int64_t id = P + run + __popc(ball & lanemask_lt()) + (head ? 1 : 0) - 1;
         if (head) a.uniq[id] = (int64_t)(((uint64_t)b << a.s) | (x[it] >> a.pbits));
         a.ti[(int64_t)(x[it] & pmask)] = id;
       }
-      run += __popc(ball[it]);
+      run += __popc(ball);
     }
   }
+  K4MARK(7);
 }
 
 __global__ void derive_entries(const int64_t* __restrict__ row1, const int64_t* __restrict__ col1,
@@ -664,14 +716,15 @@ bool convert_fast(cudaStream_t st, const int64_t* row1, const int64_t* col1, con
   if (off || n <= 0 || n > (int64_t)0x7fffffff) return false;
   const int kb = key_bits((uint64_t)(nrb * ncb - 1));
   // buckets: ~8K entries each on average (room for 2x skew below the
-  // 16K on-chip capacity), a power of two no larger than the key space
+  // 16K on-chip capacity of a K4 CTA), a power of two no larger than the
+  // key space
   int lgb = 0;
-  while (lgb < 12 && ((int64_t)1 << lgb) * 8192 < n) ++lgb;
+  while ((1 << lgb) < F_MAXB && ((int64_t)1 << lgb) * (B_CAP / 2) < n) ++lgb;
   lgb = std::min(lgb, kb);
   const int nb = 1 << lgb;
   const int s = kb - lgb;
   const int pbits = std::max(1, key_bits((uint64_t)(n - 1)));
-  if (s + pbits > 64) return false;
+  if (s + pbits >= 64) return false;   // ~0 is fast_bucket's padding sentinel
   KeyMap m{make_div(I1), make_div(J1), nrb, s, -1};
   const int lgr = key_bits((uint64_t)(nrb - 1));
   if ((nrb & (nrb - 1)) == 0 && s >= lgr) m.bc_shift = s - lgr;
@@ -681,7 +734,8 @@ bool convert_fast(cudaStream_t st, const int64_t* row1, const int64_t* col1, con
     CK(cudaFuncSetAttribute(fast_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K3_SMEM));
     CK(cudaFuncSetAttribute(fast_bucket, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K4_SMEM));
   });
-  DBuf<unsigned> thist((size_t)ntiles * nb, st), toff((size_t)ntiles * nb, st), tot(nb, st),
+  DBuf<uint16_t> thist((size_t)ntiles * nb, st), toff((size_t)ntiles * nb, st);
+  DBuf<unsigned> tot(nb, st),
       tkept(ntiles, st);
   DBuf<int64_t> bstart(nb, st), tkoff(ntiles, st), info(2, st);
   DBuf<int> zflag(1, st);
@@ -737,14 +791,27 @@ bool convert_fast(cudaStream_t st, const int64_t* row1, const int64_t* col1, con
     CK(cudaMemsetAsync(ticket.get(), 0, sizeof(unsigned), st));
     CK(cudaMemsetAsync(status.get(), 0, sizeof(unsigned long long) * nb, st));
     // group sort when the low key splits into a block-column part of at
-    // most 11 bits above the block-row bits (nrb a power of two)
+    // most B_RB bits above the block-row bits (nrb a power of two)
     int gbits = 0;
-    if ((nrb & (nrb - 1)) == 0 && s > lgr && s - lgr <= 11) gbits = s - lgr;
+    if ((nrb & (nrb - 1)) == 0 && s > lgr && s - lgr <= B_RB) gbits = s - lgr;
     BucketArgs ba{items.get(), tot.get(), bstart.get(), nb, s, pbits, gbits, ticket.get(),
                   status.get(), c.uniq.get(), c.ti.get(), rank.get()};
     fast_bucket<<<nb, B_CT, K4_SMEM, st>>>(ba);
     CK_LAUNCH();
-    note_launch(2);
+    note_launch(1);
+#ifdef MPO_CONV_PROF
+    {
+      unsigned long long hp[10];
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpyFromSymbol(hp, g_k4prof, sizeof(hp)));
+      std::fprintf(stderr, "[k4prof] cycles/bucket: load %.0f group_pass %.0f check %.0f fixup %.0f "
+                   "lsd %.0f heads %.0f lookback %.0f write %.0f\n", hp[0] / (double)nb,
+                   hp[1] / (double)nb, hp[2] / (double)nb, hp[3] / (double)nb, hp[4] / (double)nb,
+                   hp[5] / (double)nb, hp[6] / (double)nb, hp[7] / (double)nb);
+      std::memset(hp, 0, sizeof(hp));
+      CK(cudaMemcpyToSymbol(g_k4prof, hp, sizeof(hp)));
+    }
+#endif
     int zf = 0;
     CK(cudaMemcpyAsync(&c.rank, rank.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&zf, zflag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -261,3 +261,28 @@ def test_conversion_fast_and_onesweep_paths_agree():
         outs.append([z[f"arr_{k}"] for k in range(5)])
     for x, y in zip(*outs):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("order", ["shuffled", "row_sorted"])
+def test_conversion_dense_block_column(order):
+    """A block column with ~3000 entries fits one bucket but exceeds the
+    group sort's per-warp fix-up (64 items): shuffled, its group has key
+    inversions and the bucket takes the on-chip LSD passes; row-sorted, the
+    group arrives in order.  Both bit-exact against the oracle."""
+    m = _api()
+    from paper_1707_07803_b200.workloads import square_plan
+    rng = np.random.default_rng(12)
+    n = 1 << 16
+    r = np.concatenate([rng.choice(n, 3000, replace=False) + 1, rng.integers(1, n + 1, 40000)])
+    c = np.concatenate([np.full(3000, 4097, dtype=np.int64), rng.integers(1, n + 1, 40000)])
+    key = np.unique((r - 1) * n + (c - 1))
+    r, c = key // n + 1, key % n + 1
+    if order == "shuffled":
+        p = rng.permutation(r.size)
+        r, c = r[p], c[p]
+    v = rng.standard_normal(r.size)
+    plan = square_plan(16)
+    i1, j1, ti, vals, uniq = m.convert_structure(r, c, v, plan).arrays()
+    st = orc.conversion_structure(r, c, v, plan.row_factors, plan.col_factors)
+    assert np.array_equal(st.uniq, uniq) and np.array_equal(st.ti, ti)
+    assert np.array_equal(st.i1, i1) and np.array_equal(st.j1, j1)
