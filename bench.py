@@ -628,11 +628,27 @@ def bench_conversion(args, torch, dist, rank, world, dev, barrier, max_over_rank
     secs = max_over_ranks(e0.elapsed_time(e1) / 1e3) / args.steps
     blocks = res.rank
     compulsory = 32.0 * n + 8.0 * blocks   # read 24 B/nnz, write ti 8 B, uniq 8 B
+    # the same shard in shuffled order (a COO in no particular order takes the
+    # full-key in-bucket sort); reported beside the row-sorted headline
+    perm = torch.from_numpy(np.random.default_rng(1).permutation(hi - lo)).to(dev)
+    sr, sc, sv = tr[perm], tc[perm], tv[perm]
+    del perm
+    for _ in range(args.warmup):
+        convert_sharded(sr, sc, sv, plan, ops)
+    torch.cuda.synchronize()
+    barrier()
+    e0.record()
+    for _ in range(args.steps):
+        convert_sharded(sr, sc, sv, plan, ops)
+    e1.record()
+    e1.synchronize()
+    secs_shuf = max_over_ranks(e0.elapsed_time(e1) / 1e3) / args.steps
+    del sr, sc, sv
     peak_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6521.1
     achieved = compulsory / secs / 1e9 / world   # per GPU
     try:
-        ctraffic = json.load(open(os.path.join(ROOT, "profiles", "conv_traffic.json")))
+        ctraffic = json.load(open(os.path.join(ROOT, "profiles", "r02_conv_traffic.json")))
     except (OSError, ValueError):
         ctraffic = {}
     # end to end through the sharded path: this rank's host COO shard
@@ -667,6 +683,8 @@ def bench_conversion(args, torch, dist, rank, world, dev, barrier, max_over_rank
         "value": n / secs, "unit": "nnz/s", "n_gpus": world, "scaling": "strong",
         "nnz": int(n), "blocks": int(blocks), "ms_per_step": secs * 1e3,
         "input_order": "row-sorted COO (deduplicated by np.unique)",
+        "shuffled_input": {"value": n / secs_shuf, "unit": "nnz/s", "ms_per_step": secs_shuf * 1e3,
+                           "note": "same shard, randomly permuted entries"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                      "frac": achieved / peak_hbm,
                      "traffic": ctraffic.get("dram_bytes_per_step"),
