@@ -94,8 +94,21 @@ bool small_svd(cudaStream_t st, int64_t m, int64_t n, const double* M, int64_t l
 // Inverse of a k x k upper-triangular matrix, and the certified lower
 // bound 1 / ||U^{-1}||_F <= sigma_min(U) (rankcert.cu).
 void tri_inv_upper(cudaStream_t st, int64_t k, const double* U, int64_t ldu, double* Out);
+// inv_out (k x k, optional) receives U^{-1}.
 double min_sv_lower_bound(cudaStream_t st, int64_t k, const double* U, int64_t ldu,
-                          double target);
+                          double target, double* inv_out = nullptr);
+// Tail truncation of M = R'^T Q'^T (right: M = Q R') at level delta from R'
+// (k x k upper triangular) and inv = R'^{-1} (rankcert.cu): t = the number
+// of singular values _truncation_rank discards and C (k x (k - t)) an
+// orthonormal basis of the complement of their left (right: right)
+// singular vectors of R'.  false: not resolved inside the iterated block
+// (the caller takes the full SVD).
+struct TailCut {
+  int64_t t = 0;
+  DBuf<double> C;
+};
+bool tail_cut(cudaStream_t st, int64_t k, const double* Rt, int64_t ldr, const double* inv,
+              double delta, bool right, TailCut& out);
 
 }  // namespace mpob
 

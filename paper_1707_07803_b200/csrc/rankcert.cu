@@ -20,6 +20,9 @@
 // rank decision, is the same either way (the next core's unfolding changes
 // by an orthogonal factor only).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -100,15 +103,20 @@ static double host_frob(cudaStream_t st, const double* x, int64_t n, double* scr
 // carried as logarithms).  0 when U is singular or a norm overflows: the
 // caller then factors by SVD.
 double min_sv_lower_bound(cudaStream_t st, int64_t k, const double* U, int64_t ldu,
-                          double target) {
-  DBuf<double> inv((size_t)k * k, st), nrm(1, st);
-  tri_inv_upper(st, k, U, ldu, inv.get());
-  const double h = host_frob(st, inv.get(), k * k, nrm.get());
+                          double target, double* inv_out) {
+  DBuf<double> inv_own, nrm(1, st);
+  double* inv = inv_out;
+  if (!inv) {
+    inv_own.alloc((size_t)k * k, st);
+    inv = inv_own.get();
+  }
+  tri_inv_upper(st, k, U, ldu, inv);
+  const double h = host_frob(st, inv, k * k, nrm.get());
   if (!(h > 0.0) || !std::isfinite(h)) return 0.0;
   const double b1 = 1.0 / h;
   if (b1 > target || k < 256) return b1;
   DBuf<double> G((size_t)k * k, st), H((size_t)k * k, st);
-  dgemm(st, true, false, k, k, k, 1.0, inv.get(), k, inv.get(), k, 0.0, G.get(), k);
+  dgemm(st, true, false, k, k, k, 1.0, inv, k, inv, k, 0.0, G.get(), k);
   double logl = 0.0;   // log ||G^8||_F^{1/8} accumulated as sum of w_j log f_j
   double w = 1.0;
   double* a = G.get();
@@ -125,6 +133,137 @@ double min_sv_lower_bound(cudaStream_t st, int64_t k, const double* U, int64_t l
   }
   const double b2 = std::exp(-0.5 * logl);   // 1 / sqrt(lambda bound)
   return std::max(b1, b2);
+}
+
+// ---------------------------------------------------------------------------
+// Tail truncation: when the certificate fails, only the singular values
+// below (or near) delta decide _truncation_rank (mpo.py:297-304), and only
+// their directions are discarded.  With M = R'^T Q'^T (the LQ above) the
+// discarded right directions of M are Q' U_t, U_t the left singular vectors
+// of R' for its smallest singular values, and the rounded unfolding is
+//     M_r = M (I - V_t V_t^T) = (R'^T C)(Q' C)^T,   C C^T = I - U_t U_t^T,
+// the same tensor as the reference's U_r S_r Vh_r in another gauge (every
+// later singular value and rank is unchanged, as for the certificate).
+//
+// U_t and the smallest singular values come from subspace iteration with
+// (R' R'^T)^{-1} = inv^T inv on a block of p vectors (two DMMA GEMMs + a
+// QR per step) and Rayleigh-Ritz (QR of R'^T X, SVD of its p x p factor).
+// The cut is taken from the Ritz values exactly as _truncation_rank takes
+// it from the full spectrum (tail sums from the smallest value up) once it
+// lies inside the block with a margin and the block has converged: the
+// angle of the discarded directions shrinks by (a_t / a_p)^2 per step, so
+// the discarded set is resolved to rounding (the same accuracy class as
+// the reference's dgesdd subspace).  Anything else returns false and the
+// caller takes the full SVD.
+
+__device__ __forceinline__ uint64_t splitmix(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// deterministic N(0,1) start block (Box-Muller on a counter hash)
+__global__ void hash_normal_kernel(double* x, int64_t n, uint64_t seed) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = splitmix(seed ^ (2 * (uint64_t)i)), b = splitmix(seed ^ (2 * (uint64_t)i + 1));
+    const double u1 = ((a >> 11) + 1) * (1.0 / 9007199254740993.0);
+    const double u2 = (b >> 11) * (1.0 / 9007199254740992.0);
+    x[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  }
+}
+
+bool tail_cut(cudaStream_t st, int64_t k, const double* Rt, int64_t ldr, const double* inv,
+              double delta, bool right, TailCut& out) {
+  static const bool trace = std::getenv("MPO_B200_TRACE") != nullptr;
+  for (int64_t p : {(int64_t)64, (int64_t)256}) {
+    if (2 * p > k) break;
+    DBuf<double> X((size_t)k * p, st), Y((size_t)k * p, st), Rx((size_t)p * p, st);
+    {
+      const int grid = (int)std::min<int64_t>(cdiv(k * p, 256), 1024);
+      hash_normal_kernel<<<grid, 256, 0, st>>>(X.get(), k * p, 0x5eed0000ull + (uint64_t)k);
+      CK_LAUNCH();
+      note_launch();
+    }
+    std::vector<double> a(p), prev;
+    SvdOut rr;
+    int64_t t = -1;
+    bool ok = false;
+    const int maxit = p <= 64 ? 8 : 10;
+    for (int it = 0; it < maxit && !ok; ++it) {
+      // X <- orth((R' R'^T)^{-1} X) = orth(inv^T inv X)  (right: (R'^T R')^{-1} = inv inv^T)
+      dgemm(st, right, false, k, p, k, 1.0, inv, k, X.get(), k, 0.0, Y.get(), k);
+      dgemm(st, !right, false, k, p, k, 1.0, inv, k, Y.get(), k, 0.0, X.get(), k);
+      householder_qr(st, k, p, X.get(), k, Y.get(), k, Rx.get(), p);
+      std::swap(X, Y);
+      // Rayleigh-Ritz: Z = R'^T X (right: R' X) = Qz Rz, Rz = Uz S Vz^T
+      dgemm(st, !right, false, k, p, k, 1.0, Rt, ldr, X.get(), k, 0.0, Y.get(), k);
+      {
+        DBuf<double> Qz((size_t)k * p, st);
+        householder_qr(st, k, p, Y.get(), k, Qz.get(), k, Rx.get(), p);
+      }
+      rr = SvdOut();
+      // (trunc_rel 1: rotations below 64 eps ||Rz|| are skipped -- far below
+      // the eps ||M|| accuracy the cut needs; the block's values span many decades)
+      if (!small_svd(st, p, p, Rx.get(), p, rr, 1.0)) svd_thin(st, p, p, Rx.get(), p, rr, 1.0);
+      std::vector<double> sd(p);
+      CK(cudaMemcpyAsync(sd.data(), rr.s.get(), sizeof(double) * p, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int64_t j = 0; j < p; ++j) a[j] = sd[p - 1 - j];   // ascending
+      for (double v : a)
+        if (!std::isfinite(v)) return false;
+      // the cut: the largest t whose smallest-first tail sum stays <= delta^2
+      const double d2 = delta * delta;
+      double acc = 0.0;
+      t = 0;
+      while (t < p && acc + a[t] * a[t] <= d2) { acc += a[t] * a[t]; ++t; }
+      t = std::min<int64_t>(t, k - 1);   // _truncation_rank's floor of 1
+      // converged when the discarded directions' residual contamination by
+      // the kept ones outside the block, a_p (a_{t-1} / a_p)^{2(it+1)} from
+      // a random start (a_{p-1} <= a_p bounds it from above), is a thousandth
+      // of delta, and the cut did not move since the last step
+      const double aj = a[t > 0 ? t - 1 : 0], ap = a[p - 1];
+      const double decay = ap > 0.0 ? std::pow(aj / ap, 2.0 * (it + 1)) : 1.0;
+      const double contam = ap * decay * std::sqrt((double)k) * 10.0;
+      const bool same = !prev.empty() && prev[0] == (double)t;
+      const bool inside = t <= p - 8;
+      if (inside && it >= 1 && same && contam <= 1e-3 * delta) ok = true;
+      prev.assign(1, (double)t);
+      if (trace)
+        std::fprintf(stderr, "[mpo_b200] tail_cut k=%lld p=%lld it=%d t=%lld a0=%.3e a_t-1=%.3e "
+                     "a_t=%.3e a_p-1=%.3e delta=%.3e contam=%.2e%s\n", (long long)k, (long long)p,
+                     it, (long long)t, a[0], a[t > 0 ? t - 1 : 0], a[std::min<int64_t>(t, p - 1)],
+                     a[p - 1], delta, contam, ok ? " ok" : "");
+      if (!inside) break;   // the cut is not inside the block: a wider one
+      // steps still needed at the current rate (aj / ap)^2 per step: give up
+      // early when they do not fit in the budget
+      if (!ok && it >= 1 && aj > 0.0 && ap > aj) {
+        const double need = std::log(1e-3 * delta / contam) / (2.0 * std::log(aj / ap));
+        if (it + 1 + need > maxit) break;
+      }
+    }
+    if (!ok) continue;
+    out.t = t;
+    const int64_t r = k - t;
+    out.C.alloc((size_t)k * r, st);
+    if (t == 0) {
+      set_identity(st, k, k, out.C.get(), k);
+      return true;
+    }
+    // U_t = X Vz[:, p-t:p]  (the Ritz vectors of the t smallest values;
+    // Vz^T = rr.vh, p x p, ld p)
+    DBuf<double> Ut((size_t)k * t, st), Rt_((size_t)t * t, st);
+    dgemm(st, false, true, k, t, p, 1.0, X.get(), k, rr.vh.get() + (p - t), p, 0.0, Ut.get(), k);
+    // C = H [0; I_r], H the Householder reflectors of U_t
+    QrReflectors f;
+    householder_qr_keep(st, k, t, Ut.get(), k, Rt_.get(), t, f);
+    fill_zero(st, out.C.get(), k * r);
+    set_identity(st, r, r, out.C.get() + t, k);
+    qr_apply_q(st, f, out.C.get(), k, r);
+    return true;
+  }
+  return false;
 }
 
 }  // namespace mpob

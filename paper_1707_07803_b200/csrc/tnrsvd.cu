@@ -177,6 +177,8 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
   static const int64_t cert_min =
       std::getenv("MPO_B200_RANKCERT_MIN") ? std::atoll(std::getenv("MPO_B200_RANKCERT_MIN")) : 256;
   constexpr double cert_margin = 4.0;
+  static const bool tail_on =
+      std::getenv("MPO_B200_TAILCUT") ? std::atoi(std::getenv("MPO_B200_TAILCUT")) != 0 : true;
   for (size_t k = d - 1; k >= 1; --k) {
     Core& c = cores[k];
     const int64_t R = c.R, N = c.I * c.J * c.S;
@@ -193,9 +195,10 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         householder_qr(st, N, R, At.get(), N, Qt.get(), N, Rt.get(), R);
       }
       double lb;
+      DBuf<double> inv((size_t)R * R, st);
       {
         Trace tr(st, "rank_cert", R, R);
-        lb = min_sv_lower_bound(st, R, Rt.get(), R, cert_margin * delta);
+        lb = min_sv_lower_bound(st, R, Rt.get(), R, cert_margin * delta, inv.get());
       }
       if (lb > cert_margin * delta) {
         // M = R'^T Q'^T: core k <- Q'^T (orthonormal rows), core k-1 absorbs R'^T
@@ -209,6 +212,26 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         cores[k - 1] = std::move(np_);
         continue;
       }
+      // tail truncation (rankcert.cu): the discarded directions from the
+      // smallest singular values alone; M_r = (R'^T C)(Q' C)^T
+      TailCut tc;
+      bool cut;
+      {
+        Trace tr(st, "tail_cut", R, R);
+        cut = tail_on && tail_cut(st, R, Rt.get(), R, inv.get(), delta, false, tc);
+      }
+      if (cut) {
+        const int64_t rr = R - tc.t;
+        Core nc = make_core(st, rr, c.I, c.J, c.S);   // C^T Q'^T (rr x N)
+        dgemm(st, true, true, rr, N, R, 1.0, tc.C.get(), R, Qt.get(), N, 0.0, nc.p(), rr);
+        DBuf<double> T((size_t)R * rr, st);            // R'^T C
+        dgemm(st, true, false, R, rr, R, 1.0, Rt.get(), R, tc.C.get(), R, 0.0, T.get(), R);
+        Core np_ = make_core(st, pv.R, pv.I, pv.J, rr);
+        dgemm(st, false, false, Mp, rr, R, 1.0, pv.p(), Mp, T.get(), R, 0.0, np_.p(), Mp);
+        cores[k] = std::move(nc);
+        cores[k - 1] = std::move(np_);
+        continue;
+      }
     }
     if (cert_on && N >= cert_min && R > N) {
       // tall unfolding: the rank drops to N at most; if sigma_min(M) > delta
@@ -218,16 +241,39 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
       DBuf<double> Mc((size_t)R * N, st), Qm((size_t)R * N, st), Rm((size_t)N * N, st);
       copy_matrix(st, R, N, c.p(), R, Mc.get(), R);
       double lb;
+      DBuf<double> inv((size_t)N * N, st);
       {
         Trace tr(st, "rank_cert_tall", R, N);
         householder_qr(st, R, N, Mc.get(), R, Qm.get(), R, Rm.get(), N);
-        lb = min_sv_lower_bound(st, N, Rm.get(), N, cert_margin * delta);
+        lb = min_sv_lower_bound(st, N, Rm.get(), N, cert_margin * delta, inv.get());
       }
       if (lb > cert_margin * delta) {
         Core nc = make_core(st, N, c.I, c.J, c.S);
         set_identity(st, N, N, nc.p(), N);
         Core np_ = make_core(st, pv.R, pv.I, pv.J, N);
         dgemm(st, false, false, Mp, N, R, 1.0, pv.p(), Mp, c.p(), R, 0.0, np_.p(), Mp);
+        cores[k] = std::move(nc);
+        cores[k - 1] = std::move(np_);
+        continue;
+      }
+      // tail truncation on the right singular vectors of Rm (M = Qm Rm):
+      // M_r = M C C^T -- core k <- C^T, core k-1 absorbs M C
+      TailCut tc;
+      bool cut;
+      {
+        Trace tr(st, "tail_cut_tall", N, N);
+        cut = tail_on && tail_cut(st, N, Rm.get(), N, inv.get(), delta, true, tc);
+      }
+      if (cut) {
+        const int64_t rr = N - tc.t;
+        Core nc = make_core(st, rr, c.I, c.J, c.S);
+        int64_t dims[2] = {N, rr};
+        int pr[2] = {1, 0};
+        permute(st, tc.C.get(), nc.p(), 2, dims, pr);
+        DBuf<double> T((size_t)R * rr, st);   // M C
+        dgemm(st, false, false, R, rr, N, 1.0, c.p(), R, tc.C.get(), N, 0.0, T.get(), R);
+        Core np_ = make_core(st, pv.R, pv.I, pv.J, rr);
+        dgemm(st, false, false, Mp, rr, R, 1.0, pv.p(), Mp, T.get(), R, 0.0, np_.p(), Mp);
         cores[k] = std::move(nc);
         cores[k - 1] = std::move(np_);
         continue;
