@@ -311,7 +311,7 @@ def run_b200(args, rank, world, local_rank):
 
     peak = fp64_peak_tflops(torch)
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r02_traffic.json")))
     except (OSError, ValueError):
         traffic = {}
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
@@ -378,36 +378,41 @@ def run_b200(args, rank, world, local_rank):
     e2e_secs = max_over_ranks(e2.elapsed_time(e3) / 1e3) / args.steps
     e2e_value = world * flops / e2e_secs / 1e12
 
-    # roofline of the dominant kernel (CUDA events around every Jacobi round kernel)
+    # roofline of the dominant kernel family: CUDA events around every
+    # Jacobi round kernel, DGEMM launch and QR panel of one extra step
     _lib.call("mpo_b200_profile_enable", 1)
     step()
     torch.cuda.synchronize()
     prof = {}
     import ctypes as C
-    for idx, kname in enumerate(["jacobi_gram_kernel", "jacobi_eig_kernel", "jacobi_apply_kernel"]):
+    names = ["jacobi_gram_kernel", "jacobi_eig_kernel", "jacobi_apply_kernel", "dgemm_kernel",
+             "qr_panel_cluster_kernel"]
+    for idx, kname in enumerate(names):
         ms, fl, n = C.c_double(), C.c_double(), C.c_ulonglong()
         _lib.call("mpo_b200_profile_read", idx, C.byref(ms), C.byref(fl), C.byref(n))
         prof[kname] = (ms.value, fl.value, n.value)
     _lib.call("mpo_b200_profile_enable", 0)
-    dom = max(prof, key=lambda k: prof[k][0])
+    # the tensor-pipe kernel with the most time (the QR panel is latency
+    # bound: its share is reported, not a roofline)
+    dom = max(("jacobi_gram_kernel", "jacobi_apply_kernel", "dgemm_kernel"),
+              key=lambda k: prof[k][0])
     ms_d, fl_d, n_d = prof[dom]
-    if fl_d <= 0:  # eig does no GEMM-shaped work; quote the DMMA kernel with most time
-        dom = max(("jacobi_gram_kernel", "jacobi_apply_kernel"), key=lambda k: prof[k][0])
-        ms_d, fl_d, n_d = prof[dom]
     achieved = fl_d / (ms_d / 1e3) / 1e12 if ms_d > 0 else 0.0
     step_ms = per_step * 1e3
     roofline = {
         "bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-        "frac": achieved / peak if peak else None, "traffic": traffic.get("dram_bytes_per_launch"),
-        "traffic_note": ("dram read+write bytes of one k=4096 launch from the committed ncu "
-                         f"--set full capture ({traffic.get('source')}); algorithmic bytes of "
-                         f"that launch {traffic.get('algorithmic_bytes_per_launch')}")
-        if traffic else None,
+        "frac": achieved / peak if peak else None,
+        "traffic": traffic.get("dram_bytes_per_launch") if dom == traffic.get("kernel") else None,
+        "traffic_note": traffic.get("note"),
         "peak_source": "measured in this run: cuBLAS DGEMM 8192^3 (torch.matmul float64); "
                        "MEASURED_PEAKS.json has no FP64 figure",
         "avg_launch_us": 1e3 * ms_d / max(n_d, 1), "launches_per_step": n_d,
+        "flops_per_step": fl_d,
         "share_of_step": (ms_d / step_ms) if step_ms else None,
-        "jacobi_ms_per_step": {k: v[0] for k, v in prof.items()},
+        "kernel_ms_per_step": {k: v[0] for k, v in prof.items()},
+        "kernel_launches_per_step": {k: v[2] for k, v in prof.items()},
+        "timing": "CUDA events around every launch of one extra (profiling) step; each "
+                  "timed launch synchronises its stream, so shares are of serialised time",
     }
 
     line = {
@@ -433,6 +438,7 @@ def run_b200(args, rank, world, local_rank):
         line["conversion"] = bench_conversion(args, torch, dist, rank, world, dev, barrier,
                                               max_over_ranks)
     line["c1"] = bench_c1(args, torch, rank, world, barrier, max_over_ranks)
+    line["tsqr"] = bench_tsqr(args, torch, rank, world, dev, barrier, max_over_ranks)
     if not args.no_c3:
         line["tnrsvd_c3q0"] = bench_c3q0(args, torch, rank, world, barrier, max_over_ranks)
     if not args.no_batched:
@@ -463,6 +469,40 @@ def run_b200(args, rank, world, local_rank):
                 "seconds": tc, "coo_constructor_seconds": tctor}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def bench_tsqr(args, torch, rank, world, dev, barrier, max_over_ranks, m=131072, n=512):
+    """one tall unfolding (m x n, the L2R sweep's QR at
+    rsvd.py:106) whose rows are sharded over the ranks, factored by the
+    row-distributed TSQR (tsqr.py: local QR, one NCCL all-gather of the
+    n x n factors, tree QR, Q assembly).  Strong scaling: the same matrix at
+    every N.  value = the reference's QR ledger flops 2 (2 m n^2 - 2 n^3 / 3)
+    per second of device time (max over ranks)."""
+    from paper_1707_07803_b200.tsqr import DenseDeviceOps, tsqr
+    rng = np.random.default_rng(77)
+    b = np.linspace(0, m, world + 1).astype(int)
+    lo, hi = int(b[rank]), int(b[rank + 1])
+    full = rng.standard_normal((m, n))
+    a = torch.from_numpy(full[lo:hi]).to(dev)
+    del full
+    ops = DenseDeviceOps(dev.index)
+    for _ in range(max(args.warmup, 1)):
+        q, r = tsqr(a, ops)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(args.steps, 3)
+    e0.record()
+    for _ in range(reps):
+        q, r = tsqr(a, ops)
+    e1.record()
+    e1.synchronize()
+    secs = max_over_ranks(e0.elapsed_time(e1) / 1e3) / reps
+    flops = 2.0 * (2.0 * m * n * n - 2.0 * n ** 3 / 3.0)
+    return {"metric": f"row-sharded TSQR of a {m}x{n} unfolding (rsvd.py:106), ledger FP64 TFLOP/s",
+            "value": flops / secs / 1e12, "unit": "TFLOP/s", "seconds": secs, "n_gpus": world,
+            "scaling": "strong", "rows_per_rank": hi - lo,
+            "exchange": "one all-gather of the n x n R factors" if world > 1 else "none (one GPU)"}
 
 
 def bench_c1(args, torch, rank, world, barrier, max_over_ranks, steps=20):

@@ -42,8 +42,10 @@ typedef struct mpo_conv mpo_conv; /* conversion structure (sparse.py:207 result)
 const char* mpo_b200_last_error(void);
 int mpo_b200_abi_version(void);
 unsigned long long mpo_b200_launch_count(void); /* kernels launched so far */
-/* CUDA-event timing of the block-Jacobi round kernels (bench roofline):
- * which = 0 jacobi_gram, 1 jacobi_eig, 2 jacobi_apply; enable(1) resets. */
+/* CUDA-event timing per kernel family (bench roofline): which = 0
+ * jacobi_gram, 1 jacobi_eig, 2 jacobi_apply, 3 dgemm (incl. split-K
+ * reduction), 4 QR panel; enable(1) resets.  Timed launches synchronise
+ * (profiling runs only). */
 int mpo_b200_profile_enable(int on);
 int mpo_b200_profile_read(int which, double* ms, double* flops, unsigned long long* launches);
 
@@ -140,6 +142,22 @@ int mpo_keys_search(mpo_ctx* ctx, const int64_t* table, int64_t ntab, const int6
                     int64_t nq, int64_t offset, int exact, int64_t* out);
 /* ti[i] = map[ti[i]] in place (device) */
 int mpo_remap_ids(mpo_ctx* ctx, const int64_t* map, int64_t* ti, int64_t n);
+
+/* ---- dense factorisations of device matrices (column-major) -----------
+ * The local steps of the row-distributed TSQR / SVD of one tall unfolding
+ * (paper_1707_07803_b200/distributed.py tsqr, tsqr_svd), replacing the
+ * per-core np.linalg.qr at rsvd.py:106 and np.linalg.svd at rsvd.py:128 when
+ * the unfolding's rows are sharded over GPUs. */
+/* reduced QR A = Q R (m >= n; Householder, dgeqrf + dorgqr) */
+int mpo_dense_qr(mpo_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, double* q,
+                 int64_t ldq, double* r, int64_t ldr);
+/* thin SVD A = U diag(s) Vt (m >= n; s descending, U orthonormal columns) */
+int mpo_dense_svd(mpo_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda, double* s,
+                  double* u, int64_t ldu, double* vt, int64_t ldvt);
+/* C = alpha op(A) op(B) + beta C (DMMA GEMM) */
+int mpo_dense_gemm(mpo_ctx* ctx, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha,
+                   const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                   double* c, int64_t ldc);
 
 #ifdef __cplusplus
 }

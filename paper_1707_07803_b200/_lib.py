@@ -65,6 +65,13 @@ SIGNATURES = {
     "mpo_keys_lookup": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, _P]),
     "mpo_keys_search": (C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int64, C.c_int, _P]),
     "mpo_remap_ids": (C.c_int, [_P, _P, _P, C.c_int64]),
+    "mpo_dense_qr": (C.c_int, [_P, C.c_int64, C.c_int64, _P, C.c_int64, _P, C.c_int64, _P,
+                               C.c_int64]),
+    "mpo_dense_svd": (C.c_int, [_P, C.c_int64, C.c_int64, _P, C.c_int64, _P, _P, C.c_int64, _P,
+                                C.c_int64]),
+    "mpo_dense_gemm": (C.c_int, [_P, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                 C.c_double, _P, C.c_int64, _P, C.c_int64, C.c_double, _P,
+                                 C.c_int64]),
 }
 
 _lib = None

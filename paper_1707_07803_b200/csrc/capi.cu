@@ -93,7 +93,7 @@ MPO_API int mpo_b200_profile_enable(int on) {
 
 MPO_API int mpo_b200_profile_read(int which, double* ms, double* flops,
                                   unsigned long long* launches) {
-  if (which < 0 || which > 2) { g_err = "profile index out of range"; return MPO_EVALUE; }
+  if (which < 0 || which >= mpob::KernelProfile::N) { g_err = "profile index out of range"; return MPO_EVALUE; }
   *ms = mpob::g_prof.ms[which];
   *flops = mpob::g_prof.flops[which];
   *launches = mpob::g_prof.launches[which];
@@ -430,4 +430,63 @@ MPO_API int mpo_keys_search(mpo_ctx* ctx, const int64_t* table, int64_t ntab, co
 
 MPO_API int mpo_remap_ids(mpo_ctx* ctx, const int64_t* map, int64_t* ti, int64_t n) {
   return guarded(ctx, [&] { mpob::remap_ids(ctx->stream, map, ti, n); });
+}
+
+// ---- dense factorisations of device matrices (column-major) -------------
+// rsvd.py:106 / :128 on one shard of a row-distributed unfolding (the local
+// step of distributed.tsqr / tsqr_svd)
+MPO_API int mpo_dense_qr(mpo_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
+                         double* q, int64_t ldq, double* r, int64_t ldr) {
+  return guarded(ctx, [&] {
+    need(m >= n && n >= 1, "mpo_dense_qr: need m >= n >= 1");
+    need(lda >= m && ldq >= m && ldr >= n, "mpo_dense_qr: leading dimension too small");
+    cudaStream_t st = ctx->stream;
+    mpob::DBuf<double> w((size_t)m * n, st);
+    mpob::copy_matrix(st, m, n, a, lda, w.get(), m);
+    if (!mpob::small_qr(st, m, n, w.get(), m, q, ldq, r, ldr))
+      mpob::householder_qr(st, m, n, w.get(), m, q, ldq, r, ldr);
+  });
+}
+
+// thin SVD M = U diag(s) Vt of an m x n device matrix (m >= n): s descending
+// (n), U (m x n) orthonormal columns, Vt (n x n)
+MPO_API int mpo_dense_svd(mpo_ctx* ctx, int64_t m, int64_t n, const double* a, int64_t lda,
+                          double* s, double* u, int64_t ldu, double* vt, int64_t ldvt) {
+  return guarded(ctx, [&] {
+    need(m >= n && n >= 1, "mpo_dense_svd: need m >= n >= 1");
+    need(lda >= m && ldu >= m && ldvt >= n, "mpo_dense_svd: leading dimension too small");
+    cudaStream_t st = ctx->stream;
+    mpob::SvdOut o;
+    if (!mpob::small_svd(st, m, n, a, lda, o, 0.0)) mpob::svd_thin(st, m, n, a, lda, o, 0.0);
+    CK(cudaMemcpyAsync(s, o.s.get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    // U = Ucarry diag(1/s), completed to orthonormal where s == 0
+    mpob::DBuf<double> w((size_t)n * n, st);
+    if (m == n) {
+      mpob::svd_left_vectors(st, n, o.ucarry.get(), m, o.s.get(), w.get());
+      mpob::copy_matrix(st, m, n, w.get(), n, u, ldu);
+    } else {
+      // tall: U = M Vt^T diag(1/s) would lose orthogonality for tiny s; QR of
+      // M first (M = Qm Rm), then U = Qm U_R from the square factor's SVD
+      mpob::DBuf<double> qm((size_t)m * n, st), rm((size_t)n * n, st), mc((size_t)m * n, st);
+      mpob::copy_matrix(st, m, n, a, lda, mc.get(), m);
+      mpob::householder_qr(st, m, n, mc.get(), m, qm.get(), m, rm.get(), n);
+      mpob::SvdOut o2;
+      if (!mpob::small_svd(st, n, n, rm.get(), n, o2, 0.0)) mpob::svd_thin(st, n, n, rm.get(), n, o2, 0.0);
+      CK(cudaMemcpyAsync(s, o2.s.get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      mpob::svd_left_vectors(st, n, o2.ucarry.get(), n, o2.s.get(), w.get());
+      mpob::dgemm(st, false, false, m, n, n, 1.0, qm.get(), m, w.get(), n, 0.0, u, ldu);
+      o = std::move(o2);
+    }
+    mpob::copy_matrix(st, n, n, o.vh.get(), n, vt, ldvt);
+  });
+}
+
+// C = alpha op(A) op(B) + beta C on device matrices (the DMMA GEMM)
+MPO_API int mpo_dense_gemm(mpo_ctx* ctx, int ta, int tb, int64_t m, int64_t n, int64_t k,
+                           double alpha, const double* a, int64_t lda, const double* b,
+                           int64_t ldb, double beta, double* c, int64_t ldc) {
+  return guarded(ctx, [&] {
+    need(m >= 0 && n >= 0 && k >= 0, "mpo_dense_gemm: negative extent");
+    mpob::dgemm(ctx->stream, ta != 0, tb != 0, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc);
+  });
 }

@@ -250,6 +250,7 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_t k, d
     scale_matrix(st, m, n, beta, C, ldc, batch, sC);
     return;
   }
+  ProfScope prof(st, 3, 2.0 * (double)m * n * k * batch);
   GemmArgs g{m, n, k, A, lda, sA, B, ldb, sB, C, ldc, sC, alpha, beta, ta, tb, k, nullptr};
   const int64_t tiles = cdiv(m, BM) * cdiv(n, BN);
   // split-K when the output grid cannot fill the 148 SMs and K is long

@@ -7,15 +7,27 @@
 
 namespace mpob {
 
-// Optional per-kernel CUDA-event timing of the Jacobi rounds (bench.py's
-// roofline): 0 = jacobi_gram, 1 = jacobi_eig, 2 = jacobi_apply.
+// Optional per-kernel CUDA-event timing (bench.py's roofline): 0 =
+// jacobi_gram, 1 = jacobi_eig, 2 = jacobi_apply, 3 = dgemm (+ its split-K
+// reduction), 4 = QR panel.  Each timed launch synchronises its stream
+// (profiling runs only).
 struct KernelProfile {
+  static constexpr int N = 5;
   bool on = false;
-  double ms[3] = {0, 0, 0};
-  double flops[3] = {0, 0, 0};
-  unsigned long long launches[3] = {0, 0, 0};
+  double ms[N] = {};
+  double flops[N] = {};
+  unsigned long long launches[N] = {};
   void add(int k, double t, double f) { ms[k] += t; flops[k] += f; launches[k] += 1; }
-  void reset() { for (int k = 0; k < 3; ++k) { ms[k] = 0; flops[k] = 0; launches[k] = 0; } }
+  void reset() { for (int k = 0; k < N; ++k) { ms[k] = 0; flops[k] = 0; launches[k] = 0; } }
+};
+// events around one launch on st when profiling (ProfScope p(st, 3, flops))
+struct ProfScope {
+  cudaStream_t st;
+  int which;
+  double flops;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ProfScope(cudaStream_t s, int w, double f);
+  ~ProfScope();
 };
 extern KernelProfile g_prof;
 

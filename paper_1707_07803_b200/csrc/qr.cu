@@ -461,6 +461,7 @@ int panel_width(int64_t mp, int wmax) {
 static void factor_panel(cudaStream_t st, double* A, int64_t lda, int64_t mp, int w, double* V,
                          int64_t ldv, double* T, double* tau, double* part, double* wpart,
                          double* vtv, double* alpha) {
+  ProfScope prof(st, 4, 4.0 * (double)mp * w * w);   // panel Householder work
   // preferred: one thread-block cluster (<= 16 CTAs, DSMEM reductions)
   const int64_t crpc = cdiv(std::max<int64_t>(64, cdiv(mp, 16)), 8) * 8;
   const size_t csmem = (size_t)crpc * w * sizeof(double);

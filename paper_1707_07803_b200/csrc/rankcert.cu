@@ -114,26 +114,33 @@ double min_sv_lower_bound(cudaStream_t st, int64_t k, const double* U, int64_t l
   const double h = host_frob(st, inv, k * k, nrm.get());
   if (!(h > 0.0) || !std::isfinite(h)) return 0.0;
   const double b1 = 1.0 / h;
-  if (b1 > target || k < 256) return b1;
+  // sigma_min <= sqrt(k) b1: a target above that cannot be certified (the
+  // caller goes straight to the tail truncation)
+  if (b1 > target || k < 256 || std::sqrt((double)k) * b1 <= target) return b1;
   DBuf<double> G((size_t)k * k, st), H((size_t)k * k, st);
   dgemm(st, true, false, k, k, k, 1.0, inv, k, inv, k, 0.0, G.get(), k);
-  double logl = 0.0;   // log ||G^8||_F^{1/8} accumulated as sum of w_j log f_j
+  // lambda_max(G) <= ||G^m||_F^{1/m} <= k^{1/(2m)} lambda_max(G): squarings
+  // (each normalised by its Frobenius norm, the norms kept as logarithms)
+  // until the bound passes or m = 8
+  double logl = 0.0;   // log ||G^m||_F^{1/m}
   double w = 1.0;
   double* a = G.get();
   double* b = H.get();
+  double best = b1;
   for (int j = 0; j < 4; ++j) {
     const double f = host_frob(st, a, k * k, nrm.get());
-    if (!(f > 0.0) || !std::isfinite(f)) return b1;
+    if (!(f > 0.0) || !std::isfinite(f)) return best;
     logl += w * std::log(f);
-    if (j == 3) break;
+    best = std::max(best, std::exp(-0.5 * logl));
+    if (best > target || j == 3) break;
     scale_matrix(st, k, k, 1.0 / f, a, k);
     dgemm(st, false, false, k, k, k, 1.0, a, k, a, k, 0.0, b, k);
     std::swap(a, b);
     w *= 0.5;
   }
-  const double b2 = std::exp(-0.5 * logl);   // 1 / sqrt(lambda bound)
-  return std::max(b1, b2);
+  return best;
 }
+
 
 // ---------------------------------------------------------------------------
 // Tail truncation: when the certificate fails, only the singular values

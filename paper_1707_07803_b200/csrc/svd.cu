@@ -862,6 +862,23 @@ void set_smem_attrs() {
 
 KernelProfile g_prof;
 
+ProfScope::ProfScope(cudaStream_t s, int w, double f) : st(s), which(w), flops(f) {
+  if (!g_prof.on) return;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+}
+ProfScope::~ProfScope() {
+  if (!e0) return;
+  cudaEventRecord(e1, st);
+  cudaEventSynchronize(e1);
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  g_prof.add(which, ms, flops);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
 // One-sided block Jacobi on the kp x kp matrix X (in place; columns >= k
 // and rows >= k are zero).  V (kp x kp) accumulates the rotations.
 template <int JB>

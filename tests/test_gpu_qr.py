@@ -1,0 +1,40 @@
+"""The blocked Householder QR (qr.cu: TSQR panels with Householder
+reconstruction, compact-WY trailing updates) through the C-ABI mpo_qr on a
+one-core MPO, i.e. np.linalg.qr(mode="reduced") of an m x n matrix
+(rsvd.py:158-163): Q orthonormal, Q R = A, R upper triangular and equal to
+LAPACK's up to row signs -- also for rank-deficient and graded columns."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _qr(a):
+    import paper_1707_07803_b200 as m
+    mm, nn = a.shape
+    q, r = m.mpo_qr(m.Mpo([a.reshape(1, mm, nn, 1)]))
+    return q.cores[0].reshape(mm, nn), np.asarray(r)
+
+
+@pytest.mark.parametrize("shape", [(700, 96), (2048, 512), (8192, 256), (3000, 300), (520, 520)])
+def test_qr_random(shape):
+    a = np.random.default_rng(sum(shape)).standard_normal(shape)
+    q, r = _qr(a)
+    n = shape[1]
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-13 * np.sqrt(n)
+    assert np.linalg.norm(q @ r - a) <= 1e-13 * np.linalg.norm(a)
+    assert np.abs(np.tril(r, -1)).max() == 0.0
+    rl = np.linalg.qr(a, mode="r")
+    np.testing.assert_allclose(np.abs(r), np.abs(rl), atol=1e-11 * np.abs(rl).max())
+
+
+def test_qr_rank_deficient_and_graded():
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((1500, 200))
+    a[:, 7] = a[:, 3] * 2.0            # exactly dependent column
+    a[:, 50] = 0.0                     # zero column
+    a[:, 100:] *= 1e-9                 # graded block
+    q, r = _qr(a)
+    assert np.linalg.norm(q.T @ q - np.eye(200)) <= 1e-13 * np.sqrt(200)
+    assert np.linalg.norm(q @ r - a) <= 1e-13 * np.linalg.norm(a)
