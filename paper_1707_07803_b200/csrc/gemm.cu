@@ -214,23 +214,32 @@ namespace {
 // (diagnostics: which GEMM shapes the sweeps spend their DGEMM time on)
 struct GemmStats {
   std::mutex mu;
-  std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int, int>, int64_t> calls;
+  // (m, n, k, batch, ta, tb) -> (calls, device ms: each call timed with events)
+  std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int, int>, std::pair<int64_t, double>>
+      calls;
   ~GemmStats() {
     if (calls.empty()) return;
     std::vector<std::pair<double, std::string>> rows;
+    double tot = 0.0, small = 0.0;
     for (auto& kv : calls) {
       auto [m, n, k, b, ta, tb] = kv.first;
-      const double f = 2.0 * m * n * k * b * kv.second;
-      char buf[160];
-      snprintf(buf, sizeof(buf), "gemm %c%c m=%lld n=%lld k=%lld batch=%lld calls=%lld gflop=%.2f",
+      const double f = 2.0 * m * n * k * b * kv.second.first, ms = kv.second.second;
+      tot += ms;
+      if (f / kv.second.first < 2e9) small += ms;
+      char buf[200];
+      snprintf(buf, sizeof(buf),
+               "gemm %c%c m=%lld n=%lld k=%lld batch=%lld calls=%lld gflop=%.2f ms=%.3f tflops=%.1f",
                ta ? 'T' : 'N', tb ? 'T' : 'N', (long long)m, (long long)n, (long long)k,
-               (long long)b, (long long)kv.second, f / 1e9);
-      rows.emplace_back(f, buf);
+               (long long)b, (long long)kv.second.first, f / 1e9, ms, ms > 0 ? f / ms / 1e9 : 0.0);
+      rows.emplace_back(ms, buf);
     }
     std::sort(rows.begin(), rows.end(), [](auto& x, auto& y) { return x.first > y.first; });
-    for (size_t i = 0; i < rows.size() && i < 40; ++i) fprintf(stderr, "[mpo_b200] %s\n", rows[i].second.c_str());
+    fprintf(stderr, "[mpo_b200] gemm total %.1f ms over %zu shapes; calls under 2 GFLOP: %.1f ms\n",
+            tot, calls.size(), small);
+    for (size_t i = 0; i < rows.size() && i < 60; ++i) fprintf(stderr, "[mpo_b200] %s\n", rows[i].second.c_str());
   }
 };
+
 GemmStats& gemm_stats() {
   static GemmStats g;
   return g;
@@ -242,9 +251,29 @@ void dgemm(cudaStream_t st, bool ta, bool tb, int64_t m, int64_t n, int64_t k, d
            int64_t ldc, int64_t batch, int64_t sA, int64_t sB, int64_t sC) {
   if (m <= 0 || n <= 0 || batch <= 0) return;
   static const bool stats = std::getenv("MPO_B200_GEMM_STATS") != nullptr;
+  struct StatTimer {   // MPO_B200_GEMM_STATS: per-shape call count and device time
+    bool on;
+    cudaStream_t st;
+    std::tuple<int64_t, int64_t, int64_t, int64_t, int, int> key;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ~StatTimer() {
+      if (!on) return;
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      std::lock_guard<std::mutex> lk(gemm_stats().mu);
+      auto& v = gemm_stats().calls[key];
+      v.first += 1;
+      v.second += ms;
+    }
+  } stat{stats, st, {m, n, k, batch, (int)ta, (int)tb}};
   if (stats) {
-    std::lock_guard<std::mutex> lk(gemm_stats().mu);
-    gemm_stats().calls[{m, n, k, batch, (int)ta, (int)tb}] += 1;
+    CK(cudaEventCreate(&stat.e0));
+    CK(cudaEventCreate(&stat.e1));
+    CK(cudaEventRecord(stat.e0, st));
   }
   if (k <= 0) {
     scale_matrix(st, m, n, beta, C, ldc, batch, sC);

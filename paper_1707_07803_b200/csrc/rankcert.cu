@@ -71,14 +71,23 @@ void tri_inv_upper(cudaStream_t st, int64_t k, const double* U, int64_t ldu, dou
   CK_LAUNCH();
   note_launch();
   DBuf<double> tmp((size_t)k * k, st);
-  // bottom-up: [[A, B], [0, D]]^{-1} = [[A^{-1}, -A^{-1} B D^{-1}], [0, D^{-1}]]
+  // bottom-up: [[A, B], [0, D]]^{-1} = [[A^{-1}, -A^{-1} B D^{-1}], [0, D^{-1}]];
+  // the full-size pairs of one level are one strided-batched GEMM each
+  // (diagonal blocks at stride 2s (ld + 1)), a trailing partial pair alone
   for (int64_t s = TB; s < k; s *= 2) {
-    for (int64_t i = 0; i + s < k; i += 2 * s) {
-      const int64_t n1 = s, n2 = std::min(s, k - i - s);
-      // tmp = B D^{-1}  (n1 x n2)
+    const int64_t full = k / (2 * s);   // pairs with n2 == s
+    if (full > 0) {
+      const int64_t su = 2 * s * (ldu + 1), so = 2 * s * (k + 1), stp = s * s;
+      dgemm(st, false, false, s, s, s, 1.0, U + s * ldu, ldu, Out + s + s * k, k, 0.0, tmp.get(),
+            s, full, su, so, stp);
+      dgemm(st, false, false, s, s, s, -1.0, Out, k, tmp.get(), s, 0.0, Out + s * k, k, full, so,
+            stp, so);
+    }
+    const int64_t i = full * 2 * s;
+    if (i + s < k) {
+      const int64_t n1 = s, n2 = k - i - s;
       dgemm(st, false, false, n1, n2, n2, 1.0, U + i + (i + s) * ldu, ldu,
             Out + (i + s) + (i + s) * k, k, 0.0, tmp.get(), n1);
-      // top-right = -A^{-1} tmp
       dgemm(st, false, false, n1, n2, n1, -1.0, Out + i + i * k, k, tmp.get(), n1, 0.0,
             Out + i + (i + s) * k, k);
     }
