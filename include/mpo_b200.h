@@ -59,6 +59,11 @@ int mpo_ctx_destroy(mpo_ctx* ctx);
  * Validates like Mpo.__init__ (mpo.py:124-145). */
 int mpo_dev_create(mpo_ctx* ctx, int d, const int64_t* shapes, const double* const* cores,
                    int from_host, mpo_dev** out);
+/* the same from ONE packed buffer of F-ordered cores back to back (one H2D) */
+int mpo_dev_create_packed(mpo_ctx* ctx, int d, const int64_t* shapes, const double* packed,
+                          int from_host, mpo_dev** out);
+/* every core into ONE packed buffer, F-ordered cores back to back (one D2H) */
+int mpo_dev_copy_all(mpo_ctx* ctx, const mpo_dev* m, double* dst, int to_host);
 int mpo_dev_num_cores(const mpo_dev* m, int* d);
 int mpo_dev_shapes(const mpo_dev* m, int64_t* shapes /* 4*d */);
 int mpo_dev_core_ptr(const mpo_dev* m, int k, const double** dev_ptr);

@@ -35,6 +35,8 @@ SIGNATURES = {
     "mpo_ctx_synchronize": (C.c_int, [_P]),
     "mpo_ctx_destroy": (C.c_int, [_P]),
     "mpo_dev_create": (C.c_int, [_P, C.c_int, _I64P, C.POINTER(_P), C.c_int, C.POINTER(_P)]),
+    "mpo_dev_create_packed": (C.c_int, [_P, C.c_int, _I64P, _P, C.c_int, C.POINTER(_P)]),
+    "mpo_dev_copy_all": (C.c_int, [_P, _P, _P, C.c_int]),
     "mpo_dev_num_cores": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "mpo_dev_shapes": (C.c_int, [_P, _I64P]),
     "mpo_dev_core_ptr": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),

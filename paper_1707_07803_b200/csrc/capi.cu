@@ -168,6 +168,68 @@ MPO_API int mpo_dev_create(mpo_ctx* ctx, int d, const int64_t* shapes, const dou
   });
 }
 
+// all cores from ONE packed buffer (F-ordered cores back to back): one H2D
+// transfer and per-core device copies instead of one blocking pageable copy
+// per core
+MPO_API int mpo_dev_create_packed(mpo_ctx* ctx, int d, const int64_t* shapes, const double* packed,
+                                  int from_host, mpo_dev** out) {
+  return guarded(ctx, [&] {
+    need(d >= 1, "an MPO needs at least one core");
+    int64_t total = 0;
+    for (int k = 0; k < d; ++k) {
+      const int64_t* s = shapes + 4 * k;
+      for (int q = 0; q < 4; ++q)
+        if (s[q] < 1) throw mpob::ValueError("core " + std::to_string(k) + " has empty extent");
+      total += s[0] * s[1] * s[2] * s[3];
+    }
+    cudaStream_t st = ctx->stream;
+    mpob::DBuf<double> stage;
+    const double* src = packed;
+    if (from_host) {
+      stage.alloc((size_t)total, st);
+      CK(cudaMemcpyAsync(stage.get(), packed, sizeof(double) * total, cudaMemcpyHostToDevice, st));
+      src = stage.get();
+    }
+    mpob::Cores cs;
+    int64_t off = 0;
+    for (int k = 0; k < d; ++k) {
+      const int64_t* s = shapes + 4 * k;
+      mpob::Core c = mpob::make_core(st, s[0], s[1], s[2], s[3]);
+      CK(cudaMemcpyAsync(c.p(), src + off, sizeof(double) * c.size(), cudaMemcpyDeviceToDevice, st));
+      off += c.size();
+      cs.push_back(std::move(c));
+    }
+    mpob::validate_chain(cs);
+    *out = wrap(std::move(cs));
+  });
+}
+
+// every core into ONE packed buffer (F-ordered cores back to back): device
+// copies into a staging buffer and a single D2H transfer
+MPO_API int mpo_dev_copy_all(mpo_ctx* ctx, const mpo_dev* m, double* dst, int to_host) {
+  return guarded(ctx, [&] {
+    cudaStream_t st = ctx->stream;
+    int64_t total = 0;
+    for (const auto& c : m->cores) total += c.size();
+    mpob::DBuf<double> stage;
+    double* dev_dst = dst;
+    if (to_host) {
+      stage.alloc((size_t)total, st);
+      dev_dst = stage.get();
+    }
+    int64_t off = 0;
+    for (const auto& c : m->cores) {
+      CK(cudaMemcpyAsync(dev_dst + off, c.p(), sizeof(double) * c.size(), cudaMemcpyDeviceToDevice,
+                         st));
+      off += c.size();
+    }
+    if (to_host) {
+      CK(cudaMemcpyAsync(dst, stage.get(), sizeof(double) * total, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+  });
+}
+
 MPO_API int mpo_dev_num_cores(const mpo_dev* m, int* d) {
   *d = (int)m->cores.size();
   return MPO_OK;

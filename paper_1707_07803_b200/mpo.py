@@ -139,6 +139,9 @@ class Mpo:
                 f"ranks={list(self.ranks)})")
 
 
+_PACK_LIMIT = 1 << 22   # doubles (32 MB): packed single-transfer up/downloads below this
+
+
 class DeviceMpo:
     """An MPO resident in HBM (C-ABI handle ``mpo_dev``).  Cores are F-ordered
     FP64 device buffers owned by the library; freed with the handle."""
@@ -159,12 +162,20 @@ class DeviceMpo:
     def from_host(cls, m: "Mpo", device: int | None = None) -> "DeviceMpo":
         m = m.densify()
         ctx = _lib.context(device)
-        cores = [np.asfortranarray(c, dtype=np.float64) for c in m.cores]
+        cores = [np.asarray(c, dtype=np.float64) for c in m.cores]
         shapes = np.array([s for c in cores for s in c.shape], dtype=np.int64)
-        ptrs = (C.c_void_p * len(cores))(*[c.ctypes.data for c in cores])
         h = C.c_void_p()
-        _lib.call("mpo_dev_create", ctx, len(cores), shapes.ctypes.data_as(_lib._I64P),
-                  ptrs, 1, C.byref(h))
+        if sum(c.size for c in cores) <= _PACK_LIMIT:
+            # one packed upload (small MPOs: per-core transfers are latency)
+            packed = np.concatenate([c.ravel(order="F") for c in cores])
+            _lib.call("mpo_dev_create_packed", ctx, len(cores),
+                      shapes.ctypes.data_as(_lib._I64P), C.c_void_p(packed.ctypes.data), 1,
+                      C.byref(h))
+        else:
+            cores = [np.asfortranarray(c) for c in cores]
+            ptrs = (C.c_void_p * len(cores))(*[c.ctypes.data for c in cores])
+            _lib.call("mpo_dev_create", ctx, len(cores), shapes.ctypes.data_as(_lib._I64P),
+                      ptrs, 1, C.byref(h))
         return cls(h, ctx)
 
     @classmethod
@@ -199,8 +210,18 @@ class DeviceMpo:
 
     def to_host(self) -> Mpo:
         # cores stay in the device's F order (same values and shapes; a C-order
-        # copy would be a strided transpose of every core on the host)
-        return Mpo([self.core(k) for k in range(self.num_cores)])
+        # copy would be a strided transpose of every core on the host).  Small
+        # MPOs come down in ONE packed transfer, the cores as views of it.
+        sizes = [int(np.prod(s)) for s in self.shapes]
+        if sum(sizes) > _PACK_LIMIT:
+            return Mpo([self.core(k) for k in range(self.num_cores)])
+        buf = np.empty(sum(sizes), dtype=np.float64)
+        _lib.call("mpo_dev_copy_all", self.ctx, self.handle, C.c_void_p(buf.ctypes.data), 1)
+        out, off = [], 0
+        for s, n in zip(self.shapes, sizes):
+            out.append(buf[off:off + n].reshape(s, order="F"))
+            off += n
+        return Mpo(out)
 
     def free(self):
         if self.handle is not None and self.handle.value:
