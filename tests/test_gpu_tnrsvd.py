@@ -320,3 +320,37 @@ def test_c2_full_size():
     assert _ortho_err(lr.u.cores) <= 1e-12
     assert _ortho_err(lr.v.cores) <= 1e-12
     _full_size_parity("c2", a, lr)
+
+
+@pytest.mark.parametrize("knob", ["MPO_B200_TAILCUT", "MPO_B200_RANKCERT"])
+def test_c2_rounding_shortcuts_match_svd_path(knob, tmp_path):
+    """The rank certificate and the tail truncation (rankcert.cu) change
+    only the gauge of intermediate cores: config 2 with the shortcut
+    disabled (every truncation by the Jacobi SVD, the reference's dgesdd
+    path) gives the same ranks, singular values within 1e-12 and the same
+    sign-invariant probe reconstruction P^T (U S V^T) P' within 1e-11."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import paper_1707_07803_b200 as m, mpo_checks as mc;"
+        "from paper_1707_07803_b200.workloads import TNRSVD_ARGS, config_mpo;"
+        "a = config_mpo('c2'); lr = m.tnrsvd(a, **TNRSVD_ARGS['c2']);"
+        "pu = mc.probe_mpo(mc.row_dims(lr.u.cores), 8, 101);"
+        "pv = mc.probe_mpo(mc.row_dims(lr.v.cores), 8, 102);"
+        "ut = mc.probe(lr.u.cores, pu, 'cuda'); vt = mc.probe(lr.v.cores, pv, 'cuda');"
+        "np.savez(sys.argv[1], s=lr.s, ur=np.array(lr.u.ranks), vr=np.array(lr.v.ranks),"
+        " rec=ut.T @ (lr.s[:, None] * vt))")
+    import os
+    outs = []
+    for val in ("1", "0"):
+        path = str(tmp_path / f"o{val}.npz")
+        env = dict(os.environ, **{knob: val})
+        subprocess.run([sys.executable, "-c", code, path], cwd=ROOT, env=env, check=True)
+        outs.append(np.load(path))
+    on, off = outs
+    assert np.array_equal(on["ur"], off["ur"]) and np.array_equal(on["vr"], off["vr"])
+    np.testing.assert_allclose(on["s"], off["s"], rtol=1e-12)
+    r = off["rec"]
+    assert np.linalg.norm(on["rec"] - r) <= 1e-11 * np.linalg.norm(r)
