@@ -42,6 +42,9 @@ typedef struct mpo_conv mpo_conv; /* conversion structure (sparse.py:207 result)
 const char* mpo_b200_last_error(void);
 int mpo_b200_abi_version(void);
 unsigned long long mpo_b200_launch_count(void); /* kernels launched so far */
+/* how the truncating R2L steps were rounded so far (out[5]): certificate
+ * wide / tall, tail cut wide / tall, full SVD */
+int mpo_b200_round_paths(unsigned long long* out);
 /* CUDA-event timing per kernel family (bench roofline): which = 0
  * jacobi_gram, 1 jacobi_eig, 2 jacobi_apply, 3 dgemm (incl. split-K
  * reduction), 4 QR panel; enable(1) resets.  Timed launches synchronise

@@ -28,6 +28,7 @@ SIGNATURES = {
     "mpo_b200_last_error": (C.c_char_p, []),
     "mpo_b200_abi_version": (C.c_int, []),
     "mpo_b200_launch_count": (C.c_ulonglong, []),
+    "mpo_b200_round_paths": (C.c_int, [C.POINTER(C.c_ulonglong)]),
     "mpo_b200_profile_enable": (C.c_int, [C.c_int]),
     "mpo_b200_profile_read": (C.c_int, [C.c_int, _DP, _DP, C.POINTER(C.c_ulonglong)]),
     "mpo_ctx_create": (C.c_int, [C.c_int, _P, C.POINTER(_P)]),
@@ -140,6 +141,13 @@ def context(device: int | None = None):
 
 def launch_count() -> int:
     return int(load().mpo_b200_launch_count())
+
+
+def round_paths() -> dict:
+    """Counts of the truncation-step rounding paths taken so far."""
+    out = (C.c_ulonglong * 5)()
+    call("mpo_b200_round_paths", out)
+    return dict(zip(("cert", "cert_tall", "tail", "tail_tall", "svd"), (int(x) for x in out)))
 
 
 def host_empty(shape, dtype=np.float64, order="C"):

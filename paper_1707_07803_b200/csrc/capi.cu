@@ -17,6 +17,7 @@
 
 namespace mpob {
 unsigned long long g_launches = 0;
+unsigned long long g_round_paths[5] = {0, 0, 0, 0, 0};
 }
 
 struct mpo_ctx {
@@ -84,6 +85,10 @@ mpo_dev* wrap(mpob::Cores&& c) {
 MPO_API const char* mpo_b200_last_error(void) { return g_err.c_str(); }
 MPO_API int mpo_b200_abi_version(void) { return 1; }
 MPO_API unsigned long long mpo_b200_launch_count(void) { return mpob::g_launches; }
+MPO_API int mpo_b200_round_paths(unsigned long long* out) {
+  for (int i = 0; i < 5; ++i) out[i] = mpob::g_round_paths[i];
+  return MPO_OK;
+}
 
 MPO_API int mpo_b200_profile_enable(int on) {
   mpob::g_prof.on = on != 0;

@@ -99,5 +99,9 @@ inline void once_per_device(std::once_flag (&flags)[kMaxDevices], F&& fn) {
 // Count of our own kernel launches (reported by bench.py as gpu_launches).
 extern unsigned long long g_launches;
 inline void note_launch(int n = 1) { g_launches += (unsigned long long)n; }
+// how each truncating R2L step was rounded (tests / diagnostics):
+// 0 certificate (wide), 1 certificate (tall), 2 tail cut (wide), 3 tail cut
+// (tall), 4 full SVD
+extern unsigned long long g_round_paths[5];
 
 }  // namespace mpob

@@ -210,6 +210,7 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         dgemm(st, false, true, Mp, R, R, 1.0, pv.p(), Mp, Rt.get(), R, 0.0, np_.p(), Mp);
         cores[k] = std::move(nc);
         cores[k - 1] = std::move(np_);
+        ++g_round_paths[0];
         continue;
       }
       // tail truncation (rankcert.cu): the discarded directions from the
@@ -230,6 +231,7 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         dgemm(st, false, false, Mp, rr, R, 1.0, pv.p(), Mp, T.get(), R, 0.0, np_.p(), Mp);
         cores[k] = std::move(nc);
         cores[k - 1] = std::move(np_);
+        ++g_round_paths[2];
         continue;
       }
     }
@@ -254,6 +256,7 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         dgemm(st, false, false, Mp, N, R, 1.0, pv.p(), Mp, c.p(), R, 0.0, np_.p(), Mp);
         cores[k] = std::move(nc);
         cores[k - 1] = std::move(np_);
+        ++g_round_paths[1];
         continue;
       }
       // tail truncation on the right singular vectors of Rm (M = Qm Rm):
@@ -276,9 +279,11 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         dgemm(st, false, false, Mp, rr, R, 1.0, pv.p(), Mp, T.get(), R, 0.0, np_.p(), Mp);
         cores[k] = std::move(nc);
         cores[k - 1] = std::move(np_);
+        ++g_round_paths[3];
         continue;
       }
     }
+    ++g_round_paths[4];
     SvdOut o;
     {
       Trace tr(st, "svd", R, N);

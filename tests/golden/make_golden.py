@@ -327,6 +327,41 @@ def round_fixtures():
     print("round fixtures written", {k: v for k, v in out.items() if k.endswith("_ranks")})
 
 
+def tail_fixtures():
+    """mpo_round (mpo.py:323-354) by the reference on MPOs whose bond
+    spectrum has a dense tail straddling delta at ranks >= 256 -- the
+    regime of the device's rank certificate / tail truncation
+    (csrc/rankcert.cu): output ranks and dense matrices."""
+    out = {}
+    rng = np.random.default_rng(71)
+
+    def orth(m, n):
+        q, _ = np.linalg.qr(rng.standard_normal((m, n)))
+        return q
+
+    # two cores, bond 256 = min(left, right extent): A = U diag(s) V^T,
+    # s geometric from 1 to 1e-12 (about 43 values below delta at 1e-10)
+    s = 10.0 ** (-12.0 * np.arange(256) / 255)
+    u, v = orth(256, 256), orth(256, 256)
+    c0 = (u * s).reshape(1, 16, 16, 256, order="F")
+    c1 = v.T.reshape(256, 16, 16, 1, order="F")
+    # three cores: the same left factor at bond 0, a graded second bond
+    d0 = (u * s).reshape(1, 16, 16, 256, order="F")
+    d1 = rng.standard_normal((256, 2, 2, 64)) * (10.0 ** (-np.arange(64) / 8.0))
+    d2 = rng.standard_normal((64, 8, 8, 1))
+    for tag, cores in (("two", [c0, c1]), ("three", [d0, d1, d2])):
+        m = rmpo.Mpo(cores)
+        pack_cores(f"tail_{tag}_in", m.cores, out)
+        for ttag, tol in (("t10", 1e-10), ("t8", 1e-8)):
+            r = rmpo.mpo_round(m, tol)
+            out[f"tail_{tag}_{ttag}_ranks"] = np.array(r.ranks)
+            out[f"tail_{tag}_{ttag}_dense"] = rmpo.contract_to_matrix(r)
+            print(tag, ttag, r.ranks)
+        out[f"tail_{tag}_dense"] = rmpo.contract_to_matrix(m)
+    np.savez_compressed(os.path.join(HERE, "round_tail.npz"), **out)
+    print("tail fixtures written")
+
+
 def io_fixtures():
     """Reference-written .mpo and Matrix Market files (byte-compatibility
     fixtures for paper_1707_07803_b200.io)."""
@@ -346,6 +381,8 @@ if __name__ == "__main__":
         big()
     elif len(sys.argv) > 1 and sys.argv[1] == "--round":
         round_fixtures()
+    elif len(sys.argv) > 1 and sys.argv[1] == "--tail":
+        tail_fixtures()
     elif len(sys.argv) > 1 and sys.argv[1] == "--io":
         io_fixtures()
     else:

@@ -60,3 +60,24 @@ def test_capped_conversion_matches_reference(tag):
     assert got.ranks == tuple(z[p + "ranks"])
     want = z[p + "dense"]
     assert np.linalg.norm(orc.contract(got.cores) - want) <= 1e-12 * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("tag,ttag,tol", [("two", "t10", 1e-10), ("two", "t8", 1e-8),
+                                          ("three", "t10", 1e-10), ("three", "t8", 1e-8)])
+def test_mpo_round_dense_tail_matches_reference(tag, ttag, tol):
+    """Bond spectra with a dense tail straddling delta at rank 256 (the
+    rank certificate / tail truncation regime, rankcert.cu) rounded by the
+    reference's mpo_round (tests/golden/round_tail.npz): equal ranks, matrix
+    within 1e-12 relative; the two-core case at 1e-10 must take the tail
+    truncation (43 values below delta inside the 64-vector block)."""
+    m = _api()
+    from paper_1707_07803_b200 import _lib
+    z = load_golden("round_tail.npz")
+    before = _lib.round_paths()
+    got = m.mpo_round(m.Mpo(unpack_cores(z, f"tail_{tag}_in")), tol)
+    after = _lib.round_paths()
+    assert got.ranks == tuple(z[f"tail_{tag}_{ttag}_ranks"])
+    want = z[f"tail_{tag}_{ttag}_dense"]
+    assert np.linalg.norm(orc.contract(got.cores) - want) <= 1e-12 * np.linalg.norm(want)
+    if (tag, ttag) == ("two", "t10"):
+        assert after["tail"] > before["tail"], (before, after)
