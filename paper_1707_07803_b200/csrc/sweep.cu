@@ -275,6 +275,10 @@ Cores orthogonalize_product(cudaStream_t st, const Cores* a, bool ta, const Core
   for (size_t j = d - 1; j >= 1; --j) {
     const int64_t IK = P[j].I() * P[j].K(), R = P[j].R();
     const int64_t nr = IK * rr;
+    if (std::getenv("MPO_B200_TRACE"))
+      fprintf(stderr, "[mpo_b200]   pre-pass core %zu: R %lld IK %lld rr %lld left %lld -> %s\n", j,
+              (long long)R, (long long)IK, (long long)rr, (long long)left[j - 1],
+              (nr < R && nr < left[j - 1]) ? "reduce" : "stop");
     if (!(nr < R && nr < left[j - 1])) break;
     DBuf<double> Mt((size_t)(nr * R), st);
     if (j == d - 1) {
@@ -321,9 +325,13 @@ Cores orthogonalize_product(cudaStream_t st, const Cores* a, bool ta, const Core
       // pick the smaller intermediate: P x_4 Lt^T (R·IK·rr) or C x_1 P (m·IK·S)
       const int64_t IK = P[k].I() * P[k].K();
       const int64_t R = P[k].R(), S = P[k].S();
-      const bool right_first =
-          (k == 0) || right_absorb_flops(P[k], rr) + 2.0 * m * IK * rr * R <=
-                          left_absorb_flops(P[k], m) + 2.0 * m * IK * S * rr;
+      const double f_right = right_absorb_flops(P[k], rr) + 2.0 * m * IK * rr * R;
+      const double f_left = left_absorb_flops(P[k], m) + 2.0 * m * IK * S * rr;
+      const bool right_first = (k == 0) || f_right <= f_left;
+      if (tr.on)
+        fprintf(stderr, "[mpo_b200]   meet core %zu of %zu: m %lld R %lld IK %lld S %lld rr %lld, "
+                "right-first %.3g flops, left-first %.3g flops\n", k, d, (long long)m, (long long)R,
+                (long long)IK, (long long)S, (long long)rr, f_right, f_left);
       if (right_first) {
         DBuf<double> Mt((size_t)(IK * rr * R), st);
         right_absorb_t(st, P[k], Lt.get(), rr, Mt.get());
