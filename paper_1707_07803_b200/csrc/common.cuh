@@ -97,6 +97,22 @@ inline void once_per_device(std::once_flag (&flags)[kMaxDevices], F&& fn) {
 }
 
 // Count of our own kernel launches (reported by bench.py as gpu_launches).
+// MPO_CHECK builds (tools/build_variant.sh check <file> -DMPO_CHECK): device
+// bounds checks on the indexing the deterministic-output argument relies on
+// (compute-sanitizer is not available on the GPU pool); a violation traps.
+#ifdef MPO_CHECK
+#define MPO_DCHECK(cond)                                                            \
+  do {                                                                              \
+    if (!(cond)) {                                                                  \
+      printf("MPO_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+             #cond, (int)blockIdx.x, (int)threadIdx.x);                             \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define MPO_DCHECK(cond) do {} while (0)
+#endif
+
 extern unsigned long long g_launches;
 inline void note_launch(int n = 1) { g_launches += (unsigned long long)n; }
 // how each truncating R2L step was rounded (tests / diagnostics):

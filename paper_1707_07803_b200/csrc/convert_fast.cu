@@ -369,6 +369,8 @@ __global__ void __launch_bounds__(F_CT) fast_scatter(ScatterArgs a) {
         const unsigned b = (unsigned)(key >> a.m.s);
         const unsigned slot = atomicAdd(&cur[b], 1u);   // in-tile slot: order irrelevant
         const unsigned j = loff[b] + slot;
+        MPO_DCHECK(b < (unsigned)a.nb && slot < a.thist[(int64_t)blockIdx.x * a.nb + b] &&
+                   j < (unsigned)F_TILE);
         sitem[j] = ((key & lowmask) << a.pbits) | (uint64_t)pos;
         sb[j] = (uint16_t)b;
         if (a.zeros) {
@@ -386,7 +388,10 @@ __global__ void __launch_bounds__(F_CT) fast_scatter(ScatterArgs a) {
   for (int b = tid; b < nb; b += F_CT) cur[b] = (unsigned)(a.bstart[b] + trow[b]) - loff[b];
   __syncthreads();
   const unsigned cnt = s_total;
-  for (unsigned j = tid; j < cnt; j += F_CT) a.items[cur[sb[j]] + j] = sitem[j];
+  for (unsigned j = tid; j < cnt; j += F_CT) {
+    MPO_DCHECK(sb[j] < (unsigned)nb);
+    a.items[cur[sb[j]] + j] = sitem[j];
+  }
 }
 
 // ---------------- K4 -------------------------------------------------------
@@ -509,6 +514,7 @@ __device__ void stable_pass(uint64_t (&x)[B_IT], int reff, int shift, int nbits,
     if (it < reff) {
       const unsigned d = (unsigned)(x[it] >> shift) & dmask;
       const unsigned r = (it & 1) ? (rk[it >> 1] >> 16) : (rk[it >> 1] & 0xffffu);
+      MPO_DCHECK(dst0[d] + wh[warp * nbin + d] + r < (unsigned)B_CAP);
       A[dst0[d] + wh[warp * nbin + d] + r] = x[it];
     }
   }
@@ -687,6 +693,8 @@ __global__ void __launch_bounds__(B_CT, B_MINB) fast_bucket(BucketArgs a) {
       const unsigned ball = __ballot_sync(0xffffffffu, head);
       if (x[it] != ~0ull) {
         const int64_t id = P + run + __popc(ball & lanemask_lt()) + (head ? 1 : 0) - 1;
+        MPO_DCHECK(id >= 0 && id < a.bstart[a.nb - 1] + a.tot[a.nb - 1]);
+        MPO_DCHECK((int64_t)(x[it] & pmask) < a.bstart[a.nb - 1] + a.tot[a.nb - 1]);
         if (head) a.uniq[id] = (int64_t)(((uint64_t)b << a.s) | (x[it] >> a.pbits));
         a.ti[(int64_t)(x[it] & pmask)] = id;
       }
