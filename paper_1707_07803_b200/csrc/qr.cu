@@ -448,6 +448,13 @@ int max_coresident_panel_ctas(size_t smem) {
 // memory: very tall, narrow matrices (e.g. the 196608 x 48 first core of
 // config 3's B) are factored in narrower panels
 int panel_width(int64_t mp, int wmax) {
+  // prefer the cluster panel (16 CTAs, DSMEM reductions): the widest panel
+  // (>= 8 columns) whose rows fit 16 CTAs' shared memory -- a 16384-row
+  // panel of 32 columns does not, 16 columns do; the cooperative-grid panel
+  // (one grid barrier per reduction) is several times slower per column
+  const int64_t crpc = cdiv(std::max<int64_t>(64, cdiv(mp, 16)), 8) * 8;
+  for (int w = wmax; w >= 8; w = (w + 1) / 2)
+    if (crpc * w * (int64_t)sizeof(double) <= cluster_smem_limit()) return w;
   const int64_t rpc = std::max<int64_t>(32, cdiv(mp, 148));
   int w = wmax;
   while (w > 1 && rpc * w * (int64_t)sizeof(double) > panel_smem_limit()) w = (w + 1) / 2;
