@@ -1,5 +1,5 @@
-"""The blocked Householder QR (qr.cu: TSQR panels with Householder
-reconstruction, compact-WY trailing updates) through the C-ABI mpo_qr on a
+"""The blocked Householder QR (qr.cu: cluster panels, compact-WY trailing
+updates) through the C-ABI mpo_qr on a
 one-core MPO, i.e. np.linalg.qr(mode="reduced") of an m x n matrix
 (rsvd.py:158-163): Q orthonormal, Q R = A, R upper triangular and equal to
 LAPACK's up to row signs -- also for rank-deficient and graded columns."""
@@ -17,7 +17,8 @@ def _qr(a):
     return q.cores[0].reshape(mm, nn), np.asarray(r)
 
 
-@pytest.mark.parametrize("shape", [(700, 96), (2048, 512), (8192, 256), (3000, 300), (520, 520)])
+@pytest.mark.parametrize("shape", [(700, 96), (2048, 512), (8192, 256), (3000, 300), (520, 520),
+                                   (70000, 128), (40001, 1024)])
 def test_qr_random(shape):
     a = np.random.default_rng(sum(shape)).standard_normal(shape)
     q, r = _qr(a)
@@ -38,3 +39,16 @@ def test_qr_rank_deficient_and_graded():
     q, r = _qr(a)
     assert np.linalg.norm(q.T @ q - np.eye(200)) <= 1e-13 * np.sqrt(200)
     assert np.linalg.norm(q @ r - a) <= 1e-13 * np.linalg.norm(a)
+
+
+def test_qr_tall_rank_deficient():
+    """Very tall (row-block TSQR path) with dependent, zero and graded columns."""
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((50000, 96))
+    a[:, 7] = a[:, 3] * 2.0
+    a[:, 50] = 0.0
+    a[:, 60:] *= 1e-9
+    q, r = _qr(a)
+    assert np.linalg.norm(q.T @ q - np.eye(96)) <= 1e-13 * np.sqrt(96)
+    assert np.linalg.norm(q @ r - a) <= 1e-13 * np.linalg.norm(a)
+    assert np.abs(np.tril(r, -1)).max() == 0.0
