@@ -53,3 +53,21 @@ def test_tsqr_single_rank_and_dense_ops():
     x, y = rng.standard_normal((300, 70)), rng.standard_normal((70, 90))
     c = _ops().matmul(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()).cpu().numpy()
     np.testing.assert_allclose(c, x @ y, rtol=0, atol=1e-12 * np.abs(x @ y).max())
+
+
+def test_dense_svd_tall_and_square():
+    """mpo_dense_svd: square (one-sided Jacobi, U from Ucarry / s) and tall
+    (QR first, U = Q U_R) against LAPACK, incl. a rank-deficient tall case."""
+    rng = np.random.default_rng(4)
+    ops = _ops()
+    for m, n in ((300, 300), (3000, 200), (1000, 64)):
+        a = rng.standard_normal((m, n))
+        if m == 1000:
+            a[:, 10] = a[:, 2]
+        u, s, vt = ops.svd(torch.from_numpy(a).cuda())
+        u, s, vt = u.cpu().numpy(), s.cpu().numpy(), vt.cpu().numpy()
+        sl = np.linalg.svd(a, compute_uv=False)
+        np.testing.assert_allclose(s, sl, rtol=0, atol=1e-13 * sl[0])
+        assert np.linalg.norm(u.T @ u - np.eye(n)) <= 1e-12 * n
+        assert np.linalg.norm(vt @ vt.T - np.eye(n)) <= 1e-12 * n
+        assert np.linalg.norm((u * s) @ vt - a) <= 1e-13 * np.linalg.norm(a)
