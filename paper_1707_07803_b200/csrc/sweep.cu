@@ -290,21 +290,16 @@ Cores orthogonalize_product(cudaStream_t st, const Cores* a, bool ta, const Core
       Trace tr(st, "pre_absorb", R, nr);
       right_absorb_t(st, P[j], Lt.get(), rr, Mt.get());
     }
-    // Mt (nr x R), nr < R: Q (nr x nr), Rr (nr x R)
-    DBuf<double> Q((size_t)(nr * nr), st), Rr((size_t)(nr * R), st);
-    {
-      Trace tr(st, "pre_qr", nr, R);
-      householder_qr(st, nr, R, Mt.get(), nr, Q.get(), nr, Rr.get(), nr);
-    }
-    Mt.reset();
-    // core j = Q^T as (nr, I, K, rr)
+    // Mt (nr x R) is wide (nr < R): its row space already has an orthonormal
+    // basis of size nr -- the identity -- so the rank reduction needs no
+    // factorisation: core j <- I_nr as (nr, I, K, rr) (right-orthonormal),
+    // Lt <- Mt.  The reference's reduced QR (Q^T, R) of the same wide
+    // unfolding differs only by an orthogonal nr x nr gauge on the new bond.
     Core c = make_core(st, nr, P[j].I(), P[j].K(), rr);
-    int64_t dims[2] = {nr, nr};
-    int perm[2] = {1, 0};
-    permute(st, Q.get(), c.p(), 2, dims, perm);
+    set_identity(st, nr, nr, c.p(), nr);
     P[j].expl = true;
     P[j].own = std::move(c);
-    Lt = std::move(Rr);
+    Lt = std::move(Mt);
     rr = nr;
     meet = j - 1;
   }
@@ -360,6 +355,16 @@ Cores orthogonalize_product(cudaStream_t st, const Cores* a, bool ta, const Core
     }
     const int64_t rows = n.R * n.I * n.J, cols = n.S, kk = std::min(rows, cols);
     Core q = make_core(st, n.R, n.I, n.J, kk);
+    if (rows <= cols) {
+      // wide unfolding: the identity is an orthonormal basis of its column
+      // space -- core k <- I, the unfolding itself is the carried factor
+      // (the reduced QR would only add an orthogonal gauge on the bond)
+      set_identity(st, rows, rows, q.p(), rows);
+      out[k] = std::move(q);
+      C = std::move(n.buf);
+      m = rows;
+      continue;
+    }
     DBuf<double> rm((size_t)(kk * cols), st);
     {
       Trace tr(st, "l2r_qr", rows, cols);

@@ -151,14 +151,23 @@ void l2r(cudaStream_t st, Cores& cores) {
     Core& c = cores[k];
     const int64_t m = c.R * c.I * c.J, n = c.S, kk = std::min(m, n);
     Core q = make_core(st, c.R, c.I, c.J, kk);
-    DBuf<double> rm((size_t)(kk * n), st);
-    {
-      Trace tr(st, "qr", m, n);
-      householder_qr(st, m, n, c.p(), m, q.p(), m, rm.get(), kk);
-    }
     Core& nx = cores[k + 1];
     Core nn = make_core(st, kk, nx.I, nx.J, nx.S);
-    dgemm(st, false, false, kk, nx.I * nx.J * nx.S, n, 1.0, rm.get(), kk, nx.p(), n, 0.0, nn.p(), kk);
+    if (m <= n) {
+      // wide unfolding: core k <- I (an orthonormal basis of its column
+      // space), the next core absorbs the unfolding itself -- the reduced QR
+      // would only add an orthogonal gauge on the bond
+      set_identity(st, m, m, q.p(), m);
+      dgemm(st, false, false, m, nx.I * nx.J * nx.S, n, 1.0, c.p(), m, nx.p(), n, 0.0, nn.p(), m);
+    } else {
+      DBuf<double> rm((size_t)(kk * n), st);
+      {
+        Trace tr(st, "qr", m, n);
+        householder_qr(st, m, n, c.p(), m, q.p(), m, rm.get(), kk);
+      }
+      dgemm(st, false, false, kk, nx.I * nx.J * nx.S, n, 1.0, rm.get(), kk, nx.p(), n, 0.0, nn.p(),
+            kk);
+    }
     cores[k] = std::move(q);
     cores[k + 1] = std::move(nn);
   }
@@ -322,6 +331,17 @@ void r2l(cudaStream_t st, Cores& cores, bool has_tol, double tol) {
     Core& pv = cores[k - 1];
     const int64_t Mp = pv.R * pv.I * pv.J;
     const int64_t kk = std::min(N, R);
+    if (N <= R) {
+      // M^T (N x R) is wide: core k <- I_N (orthonormal rows), core k-1
+      // absorbs M itself (the RQ would only add an orthogonal bond gauge)
+      Core nc = make_core(st, N, c.I, c.J, c.S);
+      set_identity(st, N, N, nc.p(), N);
+      Core np_ = make_core(st, pv.R, pv.I, pv.J, N);
+      dgemm(st, false, false, Mp, N, R, 1.0, pv.p(), Mp, c.p(), R, 0.0, np_.p(), Mp);
+      cores[k] = std::move(nc);
+      cores[k - 1] = std::move(np_);
+      continue;
+    }
     DBuf<double> At((size_t)(N * R), st), Qt((size_t)(N * kk), st), Rt((size_t)(kk * R), st);
     int64_t dims[2] = {R, N};
     int perm[2] = {1, 0};
