@@ -186,6 +186,7 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
   static const int64_t cert_min =
       std::getenv("MPO_B200_RANKCERT_MIN") ? std::atoll(std::getenv("MPO_B200_RANKCERT_MIN")) : 256;
   constexpr double cert_margin = 4.0;
+  static const bool tr_on = std::getenv("MPO_B200_TRACE") != nullptr;
   static const bool tail_on =
       std::getenv("MPO_B200_TAILCUT") ? std::atoi(std::getenv("MPO_B200_TAILCUT")) != 0 : true;
   for (size_t k = d - 1; k >= 1; --k) {
@@ -208,6 +209,18 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
       {
         Trace tr(st, "rank_cert", R, R);
         lb = min_sv_lower_bound(st, R, Rt.get(), R, cert_margin * delta, inv.get());
+      }
+      if (tr_on) {
+        DBuf<double> nd(1, st);
+        frob_norm(st, Rt.get(), R * R, nd.get());
+        double hr = 0, hi = 0;
+        CK(cudaMemcpyAsync(&hr, nd.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        frob_norm(st, inv.get(), R * R, nd.get());
+        CK(cudaMemcpyAsync(&hi, nd.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        fprintf(stderr, "[mpo_b200]   cert R=%lld N=%lld lb/delta=%.3g kappaF=%.3g\n", (long long)R,
+                (long long)N, lb / delta, hr * hi);
       }
       if (lb > cert_margin * delta) {
         // M = R'^T Q'^T: core k <- Q'^T (orthonormal rows), core k-1 absorbs R'^T
