@@ -195,14 +195,23 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
     Core& pv = cores[k - 1];
     const int64_t Mp = pv.R * pv.I * pv.J;
     if (cert_on && R >= cert_min && R <= N) {
-      // LQ: M^T = Q' R'  (N x R, R x R)
-      DBuf<double> At((size_t)N * R, st), Qt((size_t)N * R, st), Rt((size_t)R * R, st);
+      // LQ: M^T = Q' R'  (N x R, R x R).  Square M: Q' is formed only if the
+      // tail truncation needs it (a certified square bond keeps M itself,
+      // below), its reflectors are kept instead
+      const bool square = R == N;
+      DBuf<double> At((size_t)N * R, st), Qt, Rt((size_t)R * R, st);
+      QrReflectors f;
       {
         Trace tr(st, "lq", R, N);
         int64_t dims[2] = {R, N};
         int pr[2] = {1, 0};
         permute(st, c.p(), At.get(), 2, dims, pr);
-        householder_qr(st, N, R, At.get(), N, Qt.get(), N, Rt.get(), R);
+        if (square) {
+          householder_qr_keep(st, N, R, At.get(), N, Rt.get(), R, f);
+        } else {
+          Qt.alloc((size_t)N * R, st);
+          householder_qr(st, N, R, At.get(), N, Qt.get(), N, Rt.get(), R);
+        }
       }
       double lb;
       DBuf<double> inv((size_t)R * R, st);
@@ -223,13 +232,19 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
                 (long long)N, lb / delta, hr * hi);
       }
       if (lb > cert_margin * delta) {
-        // M = R'^T Q'^T: core k <- Q'^T (orthonormal rows), core k-1 absorbs R'^T
         Core nc = make_core(st, R, c.I, c.J, c.S);
-        int64_t dims[2] = {N, R};
-        int pr[2] = {1, 0};
-        permute(st, Qt.get(), nc.p(), 2, dims, pr);
         Core np_ = make_core(st, pv.R, pv.I, pv.J, R);
-        dgemm(st, false, true, Mp, R, R, 1.0, pv.p(), Mp, Rt.get(), R, 0.0, np_.p(), Mp);
+        if (square) {
+          // core k <- I (orthogonal), core k-1 absorbs M itself
+          set_identity(st, N, N, nc.p(), N);
+          dgemm(st, false, false, Mp, N, R, 1.0, pv.p(), Mp, c.p(), R, 0.0, np_.p(), Mp);
+        } else {
+          // M = R'^T Q'^T: core k <- Q'^T (orthonormal rows), core k-1 absorbs R'^T
+          int64_t dims[2] = {N, R};
+          int pr[2] = {1, 0};
+          permute(st, Qt.get(), nc.p(), 2, dims, pr);
+          dgemm(st, false, true, Mp, R, R, 1.0, pv.p(), Mp, Rt.get(), R, 0.0, np_.p(), Mp);
+        }
         cores[k] = std::move(nc);
         cores[k - 1] = std::move(np_);
         ++g_round_paths[0];
@@ -245,6 +260,11 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
       }
       if (cut) {
         const int64_t rr = R - tc.t;
+        if (square) {   // Q' from its reflectors: Q' = H [I; 0]
+          Qt.alloc((size_t)N * R, st);
+          set_identity(st, N, R, Qt.get(), N);
+          qr_apply_q(st, f, Qt.get(), N, R);
+        }
         Core nc = make_core(st, rr, c.I, c.J, c.S);   // C^T Q'^T (rr x N)
         dgemm(st, true, true, rr, N, R, 1.0, tc.C.get(), R, Qt.get(), N, 0.0, nc.p(), rr);
         DBuf<double> T((size_t)R * rr, st);            // R'^T C
