@@ -263,12 +263,11 @@ constexpr int QRC = 512;
 constexpr int QRC_H = QRC / 256;   // row halves per column group in the dot phase
 __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs p) {
   extern __shared__ double chunk[];  // rpc x w, column-major
-  __shared__ double s_pub[2][2 * QR_NB];   // published partials (dots | row jj), by parity
   __shared__ double s_tot[2 * QR_NB];
   __shared__ double s_w[QR_NB];
   __shared__ double s_vtv[QR_NB * QR_NB];
   __shared__ double s_tau[QR_NB];
-  __shared__ double s_red[16 * 2 * QR_NB];
+  __shared__ double s_red[2][16 * 2 * QR_NB];   // per-rank partials, by column parity
   __shared__ double s_dpart[QRC_H][QR_NB];
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks(), c = (int)cluster.block_rank();
@@ -291,7 +290,6 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
   // rewrites it (column jj+2).
   for (int jj = 0; jj < w; ++jj) {
     const int ncols = w - jj;            // slot 0: column jj itself (its norm)
-    double* pub = s_pub[jj & 1];
     {
       const int grp = warp % 8, half = warp / 8, col0 = grp * 4;
       if (col0 < ncols) {
@@ -313,25 +311,26 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
     }
     const bool owner = jj >= r0 && jj < r0 + nr;
     __syncthreads();
+    // push this rank's partials (dots, row jj) into slot c of every rank's
+    // reduction buffer: remote stores ahead of the barrier, which orders
+    // them, so the sum below reads local shared memory only
+    double* red = s_red[jj & 1];
     for (int u = t; u < ncols; u += QRC) {
       double d = 0.0;
 #pragma unroll
       for (int h = 0; h < QRC_H; ++h) d += s_dpart[h][u];
-      pub[u] = d;
-      pub[QR_NB + u] = owner ? chunk[(jj - r0) + (jj + u) * ld] : 0.0;
+      const double rowv = owner ? chunk[(jj - r0) + (jj + u) * ld] : 0.0;
+      for (int rk = 0; rk < CS; ++rk) {
+        double* dst = cluster.map_shared_rank(red, rk) + c * 2 * QR_NB;
+        dst[u] = d;
+        dst[QR_NB + u] = rowv;
+      }
     }
     cluster.sync();
-    // gather every rank's partials concurrently, then sum in rank order
-    for (int idx = t; idx < CS * 2 * ncols; idx += QRC) {
-      const int rk = idx / (2 * ncols), e = idx % (2 * ncols);
-      const int slot = e < ncols ? e : QR_NB + (e - ncols);
-      s_red[rk * 2 * QR_NB + slot] = cluster.map_shared_rank(pub, rk)[slot];
-    }
-    __syncthreads();
     for (int e = t; e < 2 * ncols; e += QRC) {
       const int slot = e < ncols ? e : QR_NB + (e - ncols);
       double tot = 0.0;
-      for (int i = 0; i < CS; ++i) tot += s_red[i * 2 * QR_NB + slot];
+      for (int i = 0; i < CS; ++i) tot += red[i * 2 * QR_NB + slot];
       s_tot[slot] = tot;
     }
     __syncthreads();
