@@ -8,12 +8,17 @@
 // cores reach (65536, 1, 2, 65536) = 34 GB each and the reference dies with
 // a MemoryError.  Here:
 //
-//  1. an R2L QR pre-pass runs over the right end of the chain while it
-//     lowers a bond rank below both the product rank and the left extent
-//     (each step contracts the product core with the carried R factor
-//     without forming the core: two DMMA GEMMs), then
-//  2. the L2R Householder sweep contracts the carried R factor into each
-//     product core the same way (two GEMMs instead of materialise + GEMM).
+//  1. an R2L pre-pass runs over the right end of the chain while it lowers
+//     a bond rank below both the product rank and the left extent: each
+//     step contracts the product core with the carried factor without
+//     forming the core (two DMMA GEMMs); the transposed unfolding is wide
+//     there, so the core becomes the identity and the unfolding itself is
+//     carried on (no factorisation: a reduced QR would only add an
+//     orthogonal gauge on the new bond), then
+//  2. the L2R sweep contracts the carried factor into each product core
+//     the same way (two GEMMs instead of materialise + GEMM) and
+//     Householder-factors the tall unfoldings; wide ones again keep the
+//     identity core and carry the unfolding.
 //
 // Every bond rank is then <= min(left extent, right extent, Ra·Rb), the
 // exact rank bound; the chain is left-orthonormal exactly as after the
