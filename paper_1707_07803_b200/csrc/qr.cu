@@ -261,14 +261,121 @@ struct ClusterPanelArgs {
 // a 512-row CTA slice
 constexpr int QRC = 512;
 constexpr int QRC_H = QRC / 256;   // row halves per column group in the dot phase
+
+// Remote shared-memory stores that signal the destination CTA's mbarrier
+// (st.async ... mbarrier::complete_tx): the per-column exchange needs no
+// fence -- cluster.sync()'s release is a MEMBAR.ALL.GPU per warp, which was
+// 40 % of the panel's stall samples (profiles/r02_panel_membar.txt).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_2f64(uint32_t dst, double a, double b, uint32_t mbar) {
+  asm volatile(
+      "st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+      ::"r"(dst), "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_LOOP:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra WAIT_DONE;\n"
+      "bra WAIT_LOOP;\n"
+      "WAIT_DONE:\n"
+      "}\n" ::"r"(mbar), "r"(parity)
+      : "memory");
+}
+
+// -DMPO_QR_PROF: clock64 phase totals of cluster rank 0's thread 0, printed per launch
+#ifdef MPO_QR_PROF
+#define QPROF(i) do { if (t == 0 && c == 0) { long long now_ = clock64(); pacc[i] += now_ - plast; plast = now_; } } while (0)
+#else
+#define QPROF(i) do { } while (0)
+#endif
+
+// T = (diag(1/tau) + striu(S))^{-1} by one warp, lane i owning column i in
+// registers: x_i = tau_i, x_r = -tau_r sum_{l=r+1..i} S(r,l) x_l (r = i-1..0)
+// run in lockstep over r = 31..0 with x_l = 0 for l > i (dlarft, forward
+// columnwise; a tau_r = 0 zeroes row and column r as the recurrence does).
+// S is 32 x 32 (ld 32), zero outside the strict upper w x w part.
+__device__ void build_t_factor_warp(const double* S, const double* tau_in, int w, double* T,
+                                    double* tau_out) {
+  const int lane = threadIdx.x & 31;
+  double x[QR_NB];
+#pragma unroll
+  for (int r = QR_NB - 1; r >= 0; --r) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int l = r + 1; l < QR_NB; ++l) {
+      const double sv = S[r + l * QR_NB];
+      if (((l - r - 1) & 3) == 0) a0 = fma(sv, x[l], a0);
+      else if (((l - r - 1) & 3) == 1) a1 = fma(sv, x[l], a1);
+      else if (((l - r - 1) & 3) == 2) a2 = fma(sv, x[l], a2);
+      else a3 = fma(sv, x[l], a3);
+    }
+    const double tr = r < w ? tau_in[r] : 0.0;
+    x[r] = r == lane ? tr : (r < lane ? -tr * ((a0 + a1) + (a2 + a3)) : 0.0);
+  }
+  if (lane < w) {
+#pragma unroll
+    for (int r = 0; r < QR_NB; ++r)
+      if (r < w) T[r + lane * w] = x[r];
+    tau_out[lane] = tau_in[lane];
+  }
+}
+
+// out (32 x 32, ld 32) = strict upper part of V^T V over this CTA's nr rows,
+// V = the explicit reflectors (unit diagonal, zeros above) held column-major
+// in smem (ld rows); zero outside the w x w block.  DMMA: 16 8x8 tiles, two
+// per warp, K = rows in steps of 4.  Called by 8 warps.
+__device__ void vtv_partial_dmma32(const double* V, int ld, int nr, int w, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  const int ia = ti * 8 + (lane >> 2);
+  for (int k0 = 0; k0 < nr; k0 += 4) {
+    const int kk = k0 + (lane & 3);
+    const bool kin = kk < nr;
+    const double av = (kin && ia < w) ? V[kk + ia * ld] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int jb = (tj0 + u) * 8 + (lane >> 2);
+      const double bv = (kin && jb < w) ? V[kk + jb * ld] : 0.0;
+      dmma884(acc[u], av, bv);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int b = (tj0 + u) * 8 + 2 * (lane & 3) + e;
+      out[ia + b * QR_NB] = (ia < w && b < w && ia < b) ? acc[u][e] : 0.0;
+    }
+}
+
 __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs p) {
   extern __shared__ double chunk[];  // rpc x w, column-major
-  __shared__ double s_tot[2 * QR_NB];
   __shared__ double s_w[QR_NB];
   __shared__ double s_vtv[QR_NB * QR_NB];
-  __shared__ double s_tau[QR_NB];
-  __shared__ double s_red[2][16 * 2 * QR_NB];   // per-rank partials, by column parity
+  __shared__ double s_tau[QR_NB], s_scal[QR_NB], s_beta[QR_NB];
+  // per-rank partials by column parity: [parity][rank][column][dot, row-jj entry]
+  __shared__ __align__(16) double s_red[2][16 * QR_NB * 2];
   __shared__ double s_dpart[QRC_H][QR_NB];
+  __shared__ __align__(8) unsigned long long s_mbar[2];
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks(), c = (int)cluster.block_rank();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -276,18 +383,43 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
   const int64_t r0 = (int64_t)c * p.rpc;
   const int64_t rem = p.mp - r0;
   const int nr = rem <= 0 ? 0 : (int)(rem < p.rpc ? rem : p.rpc);
-  for (int idx = t; idx < nr * w; idx += QRC) {
-    int r = idx % nr, col = idx / nr;
-    chunk[r + col * ld] = p.A[(r0 + r) + col * p.lda];
+  if (t == 0) {
+    mbar_init(smem_addr(&s_mbar[0]), 1);
+    mbar_init(smem_addr(&s_mbar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  // One cluster barrier per column: the norm of column jj and the dots
-  // x^T a_c of its sub-diagonal part with every later panel column are
-  // reduced together (plus the owner's row-jj entries), since with
-  // v = [1; scal x] the reflector's w_c = tau (a_jj,c + scal x^T a_c).  The
-  // published partials are double-buffered by column parity: a rank reads
-  // buffer jj&1 after barrier jj and has passed barrier jj+1 before anyone
-  // rewrites it (column jj+2).
+  for (int col = warp; col < w; col += QRC / 32)
+    for (int r = lane; r < nr; r += 32) chunk[r + col * ld] = p.A[(r0 + r) + col * p.lda];
+  // rank-1 update mapping: thread = (row, column group); a CTA slice of few
+  // rows spreads each row's columns over QRC / rows_p groups
+  const int rows_p = (nr + 31) & ~31;
+  const int rstep = min(max(rows_p, 32), QRC);
+  const int ngrp = QRC / rstep;
+  const int urow = t % rstep, ugrp = t / rstep;
+  // remote addresses of this rank's slot in rank `warp`'s buffers / mbarriers
+  uint32_t rem_red[2] = {0, 0}, rem_mb[2] = {0, 0};
+  if (warp < CS) {
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      rem_red[b] = cluster_addr(smem_addr(&s_red[b][(c * QR_NB + lane) * 2]), warp);
+      rem_mb[b] = cluster_addr(smem_addr(&s_mbar[b]), warp);
+    }
+  }
+  cluster.sync();   // every rank's mbarriers are initialised before the first remote store
+#ifdef MPO_QR_PROF
+  long long pacc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, plast = clock64(), pstart = plast;
+#endif
+  // One exchange per column: the norm of column jj and the dots x^T a_c of
+  // its sub-diagonal part with every later panel column are reduced together
+  // (plus the owner's row-jj entries), since with v = [1; scal x] the
+  // reflector's w_c = tau (a_jj,c + scal x^T a_c).  Warp rk of every rank
+  // stores the rank's partials into slot c of rank rk's buffer with st.async,
+  // which counts the bytes on rank rk's mbarrier; a rank waits on its own
+  // mbarrier only.  Buffers and mbarriers alternate by column parity: rank B's
+  // buffer jj&1 is rewritten for column jj+2 by a rank A that has received
+  // B's column-(jj+1) partials, which B sent after it finished reading
+  // column jj's.  Column jj stays unscaled in shared memory (x, and a_jj on
+  // the diagonal); scal and beta are applied at the write-back.
   for (int jj = 0; jj < w; ++jj) {
     const int ncols = w - jj;            // slot 0: column jj itself (its norm)
     {
@@ -302,90 +434,125 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
               if (col0 + u < ncols) acc[u] = fma(x, chunk[r + (jj + col0 + u) * ld], acc[u]);
           }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double sum = warp_sum(acc[u]);
-          if (lane == 0 && col0 + u < ncols) s_dpart[half][col0 + u] = sum;
-        }
+        // transposing butterfly: 4 sums over 32 lanes in 6 exchanges; lane
+        // 8u ends with column col0 + u
+        const bool hi = lane & 16, mid = lane & 8;
+        double k0 = (hi ? acc[2] : acc[0]) + __shfl_xor_sync(0xffffffffu, hi ? acc[0] : acc[2], 16);
+        double k1 = (hi ? acc[3] : acc[1]) + __shfl_xor_sync(0xffffffffu, hi ? acc[1] : acc[3], 16);
+        double k = (mid ? k1 : k0) + __shfl_xor_sync(0xffffffffu, mid ? k0 : k1, 8);
+        k += __shfl_xor_sync(0xffffffffu, k, 4);
+        k += __shfl_xor_sync(0xffffffffu, k, 2);
+        k += __shfl_xor_sync(0xffffffffu, k, 1);
+        if ((lane & 7) == 0 && col0 + (lane >> 3) < ncols) s_dpart[half][col0 + (lane >> 3)] = k;
       }
     }
     const bool owner = jj >= r0 && jj < r0 + nr;
+    const uint32_t mb = smem_addr(&s_mbar[jj & 1]);
+    if (t == 0) mbar_expect_tx(mb, (uint32_t)(CS * ncols * 16));
+    QPROF(0);
     __syncthreads();
-    // push this rank's partials (dots, row jj) into slot c of every rank's
-    // reduction buffer: remote stores ahead of the barrier, which orders
-    // them, so the sum below reads local shared memory only
-    double* red = s_red[jj & 1];
-    for (int u = t; u < ncols; u += QRC) {
+    QPROF(1);
+    if (warp < CS && lane < ncols) {
       double d = 0.0;
 #pragma unroll
-      for (int h = 0; h < QRC_H; ++h) d += s_dpart[h][u];
-      const double rowv = owner ? chunk[(jj - r0) + (jj + u) * ld] : 0.0;
-      for (int rk = 0; rk < CS; ++rk) {
-        double* dst = cluster.map_shared_rank(red, rk) + c * 2 * QR_NB;
-        dst[u] = d;
-        dst[QR_NB + u] = rowv;
+      for (int h = 0; h < QRC_H; ++h) d += s_dpart[h][lane];
+      const double rowv = owner ? chunk[(jj - r0) + (jj + lane) * ld] : 0.0;
+      st_async_2f64(rem_red[jj & 1], d, rowv, rem_mb[jj & 1]);
+    }
+    QPROF(2);
+    if (warp == 0) {
+      // one warp derives the reflector: lane u sums column u's partials in a
+      // fixed (pairwise, rank-ordered) tree, lane 0's are the norm and a_jj
+      mbar_wait(mb, (jj >> 1) & 1);
+      QPROF(3);
+      const double* red = s_red[jj & 1] + lane * 2;
+      double2 v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        v[i] = i < CS ? *reinterpret_cast<const double2*>(red + i * QR_NB * 2) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int s = 1; s < 16; s <<= 1)
+#pragma unroll
+        for (int i = 0; i < 16; i += 2 * s) { v[i].x += v[i + s].x; v[i].y += v[i + s].y; }
+      const double dt = v[0].x, rt = v[0].y;
+      const double sig = __shfl_sync(0xffffffffu, dt, 0), al = __shfl_sync(0xffffffffu, rt, 0);
+      double tau = 0.0, beta = al, scal = 0.0;
+      if (sig != 0.0) {
+        const double nrm = sqrt(fma(al, al, sig));
+        beta = al >= 0.0 ? -nrm : nrm;
+        tau = (beta - al) / beta;
+        scal = 1.0 / (al - beta);
+      }
+      if (lane == 0) { s_tau[jj] = tau; s_scal[jj] = scal; s_beta[jj] = beta; }
+      else if (lane < ncols) s_w[lane] = tau * fma(scal, dt, rt);
+    }
+    QPROF(4);
+    __syncthreads();
+    QPROF(5);
+    // v = [1; scal x]; rank-1 update of the later panel columns
+    if (rows_p >= QRC) {   // tall slice: a thread per row, every column
+      for (int r = t; r < nr; r += QRC) {
+        const int64_t gr = r0 + r;
+        if (gr < jj) continue;
+        double* rowp = chunk + r + jj * ld;
+        const double v = gr > jj ? rowp[0] * s_scal[jj] : 1.0;
+#pragma unroll 4
+        for (int cc = 1; cc < ncols; ++cc) rowp[cc * ld] -= v * s_w[cc];
+      }
+    } else if (ugrp < ngrp && urow < nr) {
+      const int64_t gr = r0 + urow;
+      if (gr >= jj) {
+        double* rowp = chunk + urow + jj * ld;
+        const double v = gr > jj ? rowp[0] * s_scal[jj] : 1.0;
+        for (int cc = 1 + ugrp; cc < ncols; cc += ngrp) rowp[cc * ld] -= v * s_w[cc];
       }
     }
-    cluster.sync();
-    for (int e = t; e < 2 * ncols; e += QRC) {
-      const int slot = e < ncols ? e : QR_NB + (e - ncols);
-      double tot = 0.0;
-      for (int i = 0; i < CS; ++i) tot += red[i * 2 * QR_NB + slot];
-      s_tot[slot] = tot;
-    }
+    QPROF(6);
     __syncthreads();
-    // every thread derives the reflector (same inputs, same arithmetic)
-    const double sig = s_tot[0], al = s_tot[QR_NB];
-    double tau = 0.0, beta = al, scal = 0.0;
-    if (sig != 0.0) {
-      const double nrm = sqrt(fma(al, al, sig));
-      beta = al >= 0.0 ? -nrm : nrm;
-      tau = (beta - al) / beta;
-      scal = 1.0 / (al - beta);
-    }
-    if (t == 0) s_tau[jj] = tau;
-    for (int c = 1 + t; c < ncols; c += QRC)
-      s_w[c] = tau * fma(scal, s_tot[c], s_tot[QR_NB + c]);
-    __syncthreads();
-    // v = [1; scal x]; rank-1 update of the later panel columns
-    for (int r = t; r < nr; r += QRC) {
-      const int64_t gr = r0 + r;
-      if (gr < jj) continue;
-      double* rowp = chunk + r + jj * ld;
-      double v = 1.0;
-      if (gr > jj) { v = rowp[0] * scal; rowp[0] = v; }
-      else rowp[0] = beta;
-      for (int c = 1; c < ncols; ++c) rowp[c * ld] -= v * s_w[c];
-    }
-    __syncthreads();
+    QPROF(7);
   }
-  for (int idx = t; idx < nr * w; idx += QRC) {
-    int r = idx % nr, col = idx / nr;
-    int64_t gr = r0 + r;
-    double x = chunk[r + col * ld];
-    p.A[gr + col * p.lda] = x;
-    double v = gr > col ? x : (gr == col ? 1.0 : 0.0);
-    p.V[gr + (int64_t)col * p.ldv] = v;
-    chunk[r + col * ld] = v;
+  // write back R / the scaled reflectors, and V (unit diagonal, zeros above)
+  for (int col = warp; col < w; col += QRC / 32) {
+    const double scal = s_scal[col], beta = s_beta[col];
+    for (int r = lane; r < nr; r += 32) {
+      const int64_t gr = r0 + r;
+      const double x = chunk[r + col * ld];
+      const double a = gr > col ? x * scal : (gr == col ? beta : x);
+      p.A[gr + col * p.lda] = a;
+      const double v = gr > col ? a : (gr == col ? 1.0 : 0.0);
+      p.V[gr + (int64_t)col * p.ldv] = v;
+      chunk[r + col * ld] = v;
+    }
   }
   __syncthreads();
-  if (warp < 8) vtv_partial_dmma(chunk, ld, nr, w, s_vtv);
+  QPROF(8);
+  if (warp < 8) vtv_partial_dmma32(chunk, ld, nr, w, s_vtv);
+  QPROF(9);
   cluster.sync();
+  QPROF(10);
   if (c == 0) {
     // sum the V^T V partials (fixed rank order) in place, then dlarft
-    for (int idx = t; idx < w * w; idx += QRC) {
+    for (int idx = t; idx < QR_NB * QR_NB; idx += QRC) {
       double tot = 0.0;
       double xv[16];   // all remote loads in flight, then the rank-order sum
 #pragma unroll
       for (int i = 0; i < 16; ++i) xv[i] = i < CS ? cluster.map_shared_rank(s_vtv, i)[idx] : 0.0;
 #pragma unroll
       for (int i = 0; i < 16; ++i) tot += xv[i];
-      chunk[idx] = tot;  // reuse own chunk (already written back)
+      s_vtv[idx] = tot;
     }
-    __syncthreads();
-    build_t_factor(chunk, chunk + w * w, s_tau, w, p.T, p.tau);  // rpc >= 64 >= 2w
   }
-  cluster.sync();  // keep every CTA's shared memory alive until rank 0 is done
+  QPROF(11);
+  cluster.sync();  // the partials are read: the other ranks may exit
+  QPROF(12);
+  if (c == 0 && warp == 0) build_t_factor_warp(s_vtv, s_tau, w, p.T, p.tau);
+  QPROF(13);
+#ifdef MPO_QR_PROF
+  if (t == 0 && c == 0)
+    printf("qrprof mp=%lld w=%d nr=%d CS=%d: dots %lld syncA %lld push %lld wait %lld scal %lld syncC %lld rank1 %lld syncD %lld | wb %lld vtv %lld cs1 %lld gather %lld cs2 %lld buildT %lld total %lld\n",
+           (long long)p.mp, w, nr, CS, pacc[0], pacc[1], pacc[2], pacc[3], pacc[4], pacc[5], pacc[6], pacc[7],
+           pacc[8], pacc[9], pacc[10], pacc[11], pacc[12], pacc[13], clock64() - pstart);
+#endif
 }
 
 __global__ void extract_r_kernel(int64_t k, int64_t n, const double* A, int64_t lda, double* R,
