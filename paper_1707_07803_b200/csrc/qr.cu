@@ -250,6 +250,7 @@ struct ClusterPanelArgs {
   int64_t mp;
   int w;
   int rpc;
+  int ld;          // shared-memory leading dimension (cluster_panel_ld)
   double* V;
   int64_t ldv;
   double* T;
@@ -340,31 +341,34 @@ __device__ void build_t_factor_warp(const double* S, const double* tau_in, int w
 
 // out (32 x 32, ld 32) = strict upper part of V^T V over this CTA's nr rows,
 // V = the explicit reflectors (unit diagonal, zeros above) held column-major
-// in smem (ld rows); zero outside the w x w block.  DMMA: 16 8x8 tiles, two
-// per warp, K = rows in steps of 4.  Called by 8 warps.
+// in smem (ld rows); zero elsewhere.  DMMA: warp (ti, tj) of 4 x 4 owns one
+// 8x8 tile (the 10 with ti <= tj compute), K = rows in steps of 4 on two
+// accumulators.  Called by all 16 warps.
 __device__ void vtv_partial_dmma32(const double* V, int ld, int nr, int w, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ti = warp >> 1, tj0 = (warp & 1) * 2;
+  const int ti = warp >> 2, tj = warp & 3;
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  const int ia = ti * 8 + (lane >> 2);
-  for (int k0 = 0; k0 < nr; k0 += 4) {
-    const int kk = k0 + (lane & 3);
-    const bool kin = kk < nr;
-    const double av = (kin && ia < w) ? V[kk + ia * ld] : 0.0;
+  const int ia = ti * 8 + (lane >> 2), jb = tj * 8 + (lane >> 2);
+  if (ti <= tj && ti * 8 < w && tj * 8 < w) {
+    const double* pa = V + (lane & 3) + ia * ld;
+    const double* pb = V + (lane & 3) + jb * ld;
+    const bool ain = ia < w, bin = jb < w;
+    for (int k0 = 0; k0 < nr; k0 += 8) {
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int jb = (tj0 + u) * 8 + (lane >> 2);
-      const double bv = (kin && jb < w) ? V[kk + jb * ld] : 0.0;
-      dmma884(acc[u], av, bv);
+      for (int h = 0; h < 2; ++h) {
+        const int kk = k0 + 4 * h + (lane & 3);
+        const bool kin = kk < nr;
+        const double av = (kin && ain) ? pa[k0 + 4 * h] : 0.0;
+        const double bv = (kin && bin) ? pb[k0 + 4 * h] : 0.0;
+        dmma884(acc[h], av, bv);
+      }
     }
   }
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int b = (tj0 + u) * 8 + 2 * (lane & 3) + e;
-      out[ia + b * QR_NB] = (ia < w && b < w && ia < b) ? acc[u][e] : 0.0;
-    }
+  for (int e = 0; e < 2; ++e) {
+    const int b = tj * 8 + 2 * (lane & 3) + e;
+    out[ia + b * QR_NB] = (ia < w && b < w && ia < b) ? acc[0][e] + acc[1][e] : 0.0;
+  }
 }
 
 __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs p) {
@@ -379,7 +383,7 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks(), c = (int)cluster.block_rank();
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int w = p.w, ld = p.rpc;
+  const int w = p.w, ld = p.ld;
   const int64_t r0 = (int64_t)c * p.rpc;
   const int64_t rem = p.mp - r0;
   const int nr = rem <= 0 ? 0 : (int)(rem < p.rpc ? rem : p.rpc);
@@ -390,12 +394,6 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
   }
   for (int col = warp; col < w; col += QRC / 32)
     for (int r = lane; r < nr; r += 32) chunk[r + col * ld] = p.A[(r0 + r) + col * p.lda];
-  // rank-1 update mapping: thread = (row, column group); a CTA slice of few
-  // rows spreads each row's columns over QRC / rows_p groups
-  const int rows_p = (nr + 31) & ~31;
-  const int rstep = min(max(rows_p, 32), QRC);
-  const int ngrp = QRC / rstep;
-  const int urow = t % rstep, ugrp = t / rstep;
   // remote addresses of this rank's slot in rank `warp`'s buffers / mbarriers
   uint32_t rem_red[2] = {0, 0}, rem_mb[2] = {0, 0};
   if (warp < CS) {
@@ -420,97 +418,184 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
   // B's column-(jj+1) partials, which B sent after it finished reading
   // column jj's.  Column jj stays unscaled in shared memory (x, and a_jj on
   // the diagonal); scal and beta are applied at the write-back.
-  for (int jj = 0; jj < w; ++jj) {
-    const int ncols = w - jj;            // slot 0: column jj itself (its norm)
-    {
-      const int grp = warp % 8, half = warp / 8, col0 = grp * 4;
-      if (col0 < ncols) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int r = lane + 32 * half; r < nr; r += 32 * QRC_H) {
-          if (r0 + r > jj) {
-            const double x = chunk[r + jj * ld];
+  //
+  // One pass over the slice per column: warp (grp, half) owns 4 columns and
+  // half of the rows; it applies reflector jj to its columns (and, redundantly,
+  // to the next pivot column p = jj + 1) and accumulates the dots of the
+  // updated pivot column with its updated columns for the next exchange.
+  const int grp = warp % 8, half = warp / 8, col0 = grp * 4;
+  double* piv = chunk + (size_t)ld * w;   // [2][ld]: the current pivot column, by parity
+  for (int jj = -1; jj < w; ++jj) {
+    const int pv = jj + 1;               // pivot whose dots this pass produces
+    const int ncp = w - pv;              // columns pv .. w-1 (slot 0: its norm)
+    if (jj >= 0) {
+      const int ncols = w - jj;          // slot 0: column jj itself (its norm)
+      const bool owner = jj >= r0 && jj < r0 + nr;
+      const uint32_t mb = smem_addr(&s_mbar[jj & 1]);
+      if (t == 0) mbar_expect_tx(mb, (uint32_t)(CS * ncols * 16));
+      QPROF(0);
+      __syncthreads();
+      QPROF(1);
+      if (warp < CS && lane < ncols) {
+        double d = 0.0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (col0 + u < ncols) acc[u] = fma(x, chunk[r + (jj + col0 + u) * ld], acc[u]);
+        for (int h = 0; h < QRC_H; ++h) d += s_dpart[h][lane];
+        const double rowv = !owner ? 0.0 : (lane == 0 ? piv[(jj & 1) * ld + (jj - r0)]
+                                                      : chunk[(jj - r0) + (jj + lane) * ld]);
+        st_async_2f64(rem_red[jj & 1], d, rowv, rem_mb[jj & 1]);
+      }
+      QPROF(2);
+      if (warp == 0) {
+        // one warp derives the reflector: lane u sums column u's partials in a
+        // fixed (pairwise, rank-ordered) tree, lane 0's are the norm and a_jj
+        mbar_wait(mb, (jj >> 1) & 1);
+        QPROF(3);
+        const double* red = s_red[jj & 1] + lane * 2;
+        double2 v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          v[i] = i < CS ? *reinterpret_cast<const double2*>(red + i * QR_NB * 2) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int s = 1; s < 16; s <<= 1)
+#pragma unroll
+          for (int i = 0; i < 16; i += 2 * s) { v[i].x += v[i + s].x; v[i].y += v[i + s].y; }
+        const double dt = v[0].x, rt = v[0].y;
+        const double sig = __shfl_sync(0xffffffffu, dt, 0), al = __shfl_sync(0xffffffffu, rt, 0);
+        double tau = 0.0, beta = al, scal = 0.0;
+        if (sig != 0.0) {
+          const double nrm = sqrt(fma(al, al, sig));
+          beta = al >= 0.0 ? -nrm : nrm;
+          tau = (beta - al) / beta;
+          scal = 1.0 / (al - beta);
+        }
+        if (lane == 0) { s_tau[jj] = tau; s_scal[jj] = scal; s_beta[jj] = beta; }
+        else if (lane < ncols) s_w[lane] = tau * fma(scal, dt, rt);
+      }
+      QPROF(4);
+      __syncthreads();
+      QPROF(5);
+    }
+    if (ncp > 0 && col0 < ncp) {
+      // reflector jj (none for jj = -1): v = [1; scal x], w as s_w.  The
+      // updated pivot column goes to piv[pv & 1] (rows >= jj), not in place:
+      // every group reads its old values in this pass.  Group 0 moves column
+      // jj from piv[jj & 1] to its final home in the slice as it reads it.
+      const bool refl = jj >= 0, g0 = col0 == 0;
+      const double scal = refl ? s_scal[jj] : 0.0;
+      const double wp = refl ? s_w[1] : 0.0;
+      const int nu = min(4, ncp - col0);   // this group's live columns
+      double wu[4], acc[4] = {0.0, 0.0, 0.0, 0.0};
+      double* cp[4];                       // dead columns alias the last live one (loads only)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        wu[u] = (refl && u < nu) ? s_w[1 + col0 + u] : 0.0;
+        cp[u] = chunk + (pv + col0 + min(u, nu - 1)) * ld;
+      }
+      const double* xj = piv + (jj & 1) * ld;
+      double* xhome = chunk + (refl ? jj : 0) * ld;
+      double* ynew = piv + (pv & 1) * ld;
+      const double* yp = chunk + pv * ld;
+      // two 32-row blocks per trip, every load ahead of the arithmetic and
+      // the stores (the compiler cannot hoist loads over the stores itself).
+      // Blocks that are full and entirely below row pv (all but the slice's
+      // last block and cluster rank 0's first) take a predicate-free path:
+      // the pass is bound by instruction issue, not by shared-memory bandwidth.
+      const int ir0 = (int)r0;
+      for (int rb = lane + 32 * half; rb < nr; rb += 64 * QRC_H) {
+        const int rbase = rb - lane;
+        if (refl && ir0 + rbase > pv && rbase + 32 * QRC_H + 32 <= nr) {
+          double x[2], yo[2], a[2][4];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int r = rb + 32 * QRC_H * k;
+            x[k] = xj[r];
+            yo[k] = yp[r];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[k][u] = cp[u][r];
+          }
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int r = rb + 32 * QRC_H * k;
+            const double v = x[k] * scal;
+            const double y = fma(-v, wp, yo[k]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[k][u] = fma(-v, wu[u], a[k][u]);
+            if (g0) {
+              a[k][0] = y;
+              ynew[r] = y;
+              xhome[r] = x[k];
+            } else {
+              cp[0][r] = a[k][0];
+            }
+            if (nu > 1) cp[1][r] = a[k][1];
+            if (nu > 2) cp[2][r] = a[k][2];
+            if (nu > 3) cp[3][r] = a[k][3];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(y, a[k][u], acc[u]);
+          }
+          continue;
+        }
+        double x[2], yo[2], a[2][4];
+        bool live[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int r = rb + 32 * QRC_H * k;
+          live[k] = r < nr;
+          const int rr = live[k] ? r : rb;
+          x[k] = refl ? xj[rr] : 0.0;
+          yo[k] = yp[rr];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a[k][u] = cp[u][rr];
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int r = rb + 32 * QRC_H * k;
+          const int gr = ir0 + r;
+          if (!live[k]) continue;
+          if (gr < jj) {
+            if (g0 && gr == jj - 1) xhome[r] = x[k];
+            continue;
+          }
+          const double v = !refl ? 0.0 : (gr > jj ? x[k] * scal : 1.0);
+          const double y = fma(-v, wp, yo[k]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a[k][u] = fma(-v, wu[u], a[k][u]);
+          if (g0) {
+            a[k][0] = y;
+            ynew[r] = y;
+            if (refl) xhome[r] = x[k];
+          } else if (refl) {
+            cp[0][r] = a[k][0];
+          }
+          if (refl) {
+            if (nu > 1) cp[1][r] = a[k][1];
+            if (nu > 2) cp[2][r] = a[k][2];
+            if (nu > 3) cp[3][r] = a[k][3];
+          }
+          if (gr > pv) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(y, a[k][u], acc[u]);
           }
         }
-        // transposing butterfly: 4 sums over 32 lanes in 6 exchanges; lane
-        // 8u ends with column col0 + u
-        const bool hi = lane & 16, mid = lane & 8;
-        double k0 = (hi ? acc[2] : acc[0]) + __shfl_xor_sync(0xffffffffu, hi ? acc[0] : acc[2], 16);
-        double k1 = (hi ? acc[3] : acc[1]) + __shfl_xor_sync(0xffffffffu, hi ? acc[1] : acc[3], 16);
-        double k = (mid ? k1 : k0) + __shfl_xor_sync(0xffffffffu, mid ? k0 : k1, 8);
-        k += __shfl_xor_sync(0xffffffffu, k, 4);
-        k += __shfl_xor_sync(0xffffffffu, k, 2);
-        k += __shfl_xor_sync(0xffffffffu, k, 1);
-        if ((lane & 7) == 0 && col0 + (lane >> 3) < ncols) s_dpart[half][col0 + (lane >> 3)] = k;
       }
-    }
-    const bool owner = jj >= r0 && jj < r0 + nr;
-    const uint32_t mb = smem_addr(&s_mbar[jj & 1]);
-    if (t == 0) mbar_expect_tx(mb, (uint32_t)(CS * ncols * 16));
-    QPROF(0);
-    __syncthreads();
-    QPROF(1);
-    if (warp < CS && lane < ncols) {
-      double d = 0.0;
-#pragma unroll
-      for (int h = 0; h < QRC_H; ++h) d += s_dpart[h][lane];
-      const double rowv = owner ? chunk[(jj - r0) + (jj + lane) * ld] : 0.0;
-      st_async_2f64(rem_red[jj & 1], d, rowv, rem_mb[jj & 1]);
-    }
-    QPROF(2);
-    if (warp == 0) {
-      // one warp derives the reflector: lane u sums column u's partials in a
-      // fixed (pairwise, rank-ordered) tree, lane 0's are the norm and a_jj
-      mbar_wait(mb, (jj >> 1) & 1);
-      QPROF(3);
-      const double* red = s_red[jj & 1] + lane * 2;
-      double2 v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        v[i] = i < CS ? *reinterpret_cast<const double2*>(red + i * QR_NB * 2) : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int s = 1; s < 16; s <<= 1)
-#pragma unroll
-        for (int i = 0; i < 16; i += 2 * s) { v[i].x += v[i + s].x; v[i].y += v[i + s].y; }
-      const double dt = v[0].x, rt = v[0].y;
-      const double sig = __shfl_sync(0xffffffffu, dt, 0), al = __shfl_sync(0xffffffffu, rt, 0);
-      double tau = 0.0, beta = al, scal = 0.0;
-      if (sig != 0.0) {
-        const double nrm = sqrt(fma(al, al, sig));
-        beta = al >= 0.0 ? -nrm : nrm;
-        tau = (beta - al) / beta;
-        scal = 1.0 / (al - beta);
-      }
-      if (lane == 0) { s_tau[jj] = tau; s_scal[jj] = scal; s_beta[jj] = beta; }
-      else if (lane < ncols) s_w[lane] = tau * fma(scal, dt, rt);
-    }
-    QPROF(4);
-    __syncthreads();
-    QPROF(5);
-    // v = [1; scal x]; rank-1 update of the later panel columns
-    if (rows_p >= QRC) {   // tall slice: a thread per row, every column
-      for (int r = t; r < nr; r += QRC) {
-        const int64_t gr = r0 + r;
-        if (gr < jj) continue;
-        double* rowp = chunk + r + jj * ld;
-        const double v = gr > jj ? rowp[0] * s_scal[jj] : 1.0;
-#pragma unroll 4
-        for (int cc = 1; cc < ncols; ++cc) rowp[cc * ld] -= v * s_w[cc];
-      }
-    } else if (ugrp < ngrp && urow < nr) {
-      const int64_t gr = r0 + urow;
-      if (gr >= jj) {
-        double* rowp = chunk + urow + jj * ld;
-        const double v = gr > jj ? rowp[0] * s_scal[jj] : 1.0;
-        for (int cc = 1 + ugrp; cc < ncols; cc += ngrp) rowp[cc * ld] -= v * s_w[cc];
-      }
+      // transposing butterfly: 4 sums over 32 lanes in 6 exchanges; lane
+      // 8u ends with column col0 + u
+      const bool hi = lane & 16, mid = lane & 8;
+      double k0 = (hi ? acc[2] : acc[0]) + __shfl_xor_sync(0xffffffffu, hi ? acc[0] : acc[2], 16);
+      double k1 = (hi ? acc[3] : acc[1]) + __shfl_xor_sync(0xffffffffu, hi ? acc[1] : acc[3], 16);
+      double k = (mid ? k1 : k0) + __shfl_xor_sync(0xffffffffu, mid ? k0 : k1, 8);
+      k += __shfl_xor_sync(0xffffffffu, k, 4);
+      k += __shfl_xor_sync(0xffffffffu, k, 2);
+      k += __shfl_xor_sync(0xffffffffu, k, 1);
+      if ((lane & 7) == 0 && col0 + (lane >> 3) < ncp) s_dpart[half][col0 + (lane >> 3)] = k;
     }
     QPROF(6);
-    __syncthreads();
-    QPROF(7);
   }
+  __syncthreads();
+  // the last pivot column's rows >= w - 2 are still in piv
+  for (int r = t; r < nr; r += QRC)
+    if (r0 + r >= w - 2) chunk[r + (w - 1) * ld] = piv[((w - 1) & 1) * ld + r];
+  __syncthreads();
   // write back R / the scaled reflectors, and V (unit diagonal, zeros above)
   for (int col = warp; col < w; col += QRC / 32) {
     const double scal = s_scal[col], beta = s_beta[col];
@@ -526,13 +611,14 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
   }
   __syncthreads();
   QPROF(8);
-  if (warp < 8) vtv_partial_dmma32(chunk, ld, nr, w, s_vtv);
+  vtv_partial_dmma32(chunk, ld, nr, w, s_vtv);
   QPROF(9);
   cluster.sync();
   QPROF(10);
   if (c == 0) {
     // sum the V^T V partials (fixed rank order) in place, then dlarft
     for (int idx = t; idx < QR_NB * QR_NB; idx += QRC) {
+      if ((idx & (QR_NB - 1)) >= (idx / QR_NB) || (idx / QR_NB) >= w) continue;   // strict upper part only
       double tot = 0.0;
       double xv[16];   // all remote loads in flight, then the rank-order sum
 #pragma unroll
@@ -549,7 +635,7 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
   QPROF(13);
 #ifdef MPO_QR_PROF
   if (t == 0 && c == 0)
-    printf("qrprof mp=%lld w=%d nr=%d CS=%d: dots %lld syncA %lld push %lld wait %lld scal %lld syncC %lld rank1 %lld syncD %lld | wb %lld vtv %lld cs1 %lld gather %lld cs2 %lld buildT %lld total %lld\n",
+    printf("qrprof mp=%lld w=%d nr=%d CS=%d: fusedtail %lld syncA %lld push %lld wait %lld scal %lld syncC %lld fused %lld (unused %lld) | wb %lld vtv %lld cs1 %lld gather %lld cs2 %lld buildT %lld total %lld\n",
            (long long)p.mp, w, nr, CS, pacc[0], pacc[1], pacc[2], pacc[3], pacc[4], pacc[5], pacc[6], pacc[7],
            pacc[8], pacc[9], pacc[10], pacc[11], pacc[12], pacc[13], clock64() - pstart);
 #endif
@@ -610,6 +696,13 @@ int max_coresident_panel_ctas(size_t smem) {
   return std::max(1, per) * nsm;
 }
 
+// rows per CTA of the cluster panel, and the shared-memory leading dimension
+// of its slice: the smallest ld >= rpc with ld = 4 (mod 16), so the DMMA
+// fragment loads of V^T V (4 consecutive rows x 8 columns per warp) take the
+// minimal two wavefronts instead of an 8-way bank conflict
+int64_t cluster_panel_rpc(int64_t mp) { return cdiv(std::max<int64_t>(64, cdiv(mp, 16)), 8) * 8; }
+int64_t cluster_panel_ld(int64_t rpc) { return rpc + ((4 - rpc % 16) + 16) % 16; }
+
 // widest panel (<= wmax columns) whose rows fit the panel kernels' shared
 // memory: very tall, narrow matrices (e.g. the 196608 x 48 first core of
 // config 3's B) are factored in narrower panels
@@ -618,9 +711,9 @@ int panel_width(int64_t mp, int wmax) {
   // (>= 8 columns) whose rows fit 16 CTAs' shared memory -- a 16384-row
   // panel of 32 columns does not, 16 columns do; the cooperative-grid panel
   // (one grid barrier per reduction) is several times slower per column
-  const int64_t crpc = cdiv(std::max<int64_t>(64, cdiv(mp, 16)), 8) * 8;
+  const int64_t crpc = cluster_panel_rpc(mp);
   for (int w = wmax; w >= 8; w = (w + 1) / 2)
-    if (crpc * w * (int64_t)sizeof(double) <= cluster_smem_limit()) return w;
+    if (cluster_panel_ld(crpc) * (w + 2) * (int64_t)sizeof(double) <= cluster_smem_limit()) return w;
   const int64_t rpc = std::max<int64_t>(32, cdiv(mp, 148));
   int w = wmax;
   while (w > 1 && rpc * w * (int64_t)sizeof(double) > panel_smem_limit()) w = (w + 1) / 2;
@@ -636,11 +729,11 @@ static void factor_panel(cudaStream_t st, double* A, int64_t lda, int64_t mp, in
                          double* vtv, double* alpha) {
   ProfScope prof(st, 4, 4.0 * (double)mp * w * w);   // panel Householder work
   // preferred: one thread-block cluster (<= 16 CTAs, DSMEM reductions)
-  const int64_t crpc = cdiv(std::max<int64_t>(64, cdiv(mp, 16)), 8) * 8;
-  const size_t csmem = (size_t)crpc * w * sizeof(double);
+  const int64_t crpc = cluster_panel_rpc(mp), cld = cluster_panel_ld(crpc);
+  const size_t csmem = (size_t)cld * (w + 2) * sizeof(double);   // slice + two pivot columns
   if ((int64_t)csmem <= cluster_smem_limit()) {
     const int CS = (int)cdiv(mp, crpc);
-    ClusterPanelArgs ca{A, lda, mp, w, (int)crpc, V, ldv, T, tau};
+    ClusterPanelArgs ca{A, lda, mp, w, (int)crpc, (int)cld, V, ldv, T, tau};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CS);
     cfg.blockDim = dim3(QRC);
