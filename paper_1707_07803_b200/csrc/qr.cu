@@ -641,6 +641,126 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
 #endif
 }
 
+// In-block update of a panel's reflectors on the rest of their outer block,
+// A_r <- (I - V T V^T)^T A_r = A_r - V T^T (V^T A_r), in ONE launch instead of
+// three skinny GEMMs (K = panel height for an output of 32 x <= 96: 7-13 us
+// each on the panel chain).  Column slabs of 8 x clusters of R CTAs along the
+// rows: a CTA forms its rows' part of W = V^T A_r (32 x 8, DMMA, fragments
+// straight from L2), the cluster all-gathers the partials with st.async on
+// each rank's mbarrier (fixed rank-order sum), then every CTA applies
+// A_r -= V (T^T W) to its rows.
+struct InblockArgs {
+  const double* V;   // mp x wi, ld ldv (unit diagonal, zeros above)
+  int64_t ldv;
+  const double* T;   // wi x wi upper triangular, ld wi
+  int wi;
+  double* A;         // mp x rem, ld lda
+  int64_t lda;
+  int64_t mp;
+  int rem;
+  int rpc;           // rows per CTA
+};
+constexpr int IBT = 256;
+__global__ void __launch_bounds__(IBT) qr_inblock_cluster_kernel(InblockArgs p) {
+  __shared__ double s_part[2][QR_NB * 8];
+  __shared__ double s_all[8][QR_NB * 8];
+  __shared__ double s_W[QR_NB * 8], s_W2[QR_NB * 8];
+  __shared__ double s_T[QR_NB * QR_NB];
+  __shared__ __align__(8) unsigned long long s_mbar;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int R = (int)cluster.num_blocks(), q = (int)cluster.block_rank();
+  const int slab = blockIdx.x / R;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int wi = p.wi, n0 = slab * 8, ncol = min(8, p.rem - n0);
+  const int64_t rbeg = (int64_t)q * p.rpc, rend = min(p.mp, rbeg + p.rpc);
+  const uint32_t mb = smem_addr(&s_mbar);
+  if (t == 0) {
+    mbar_init(mb, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(mb, (uint32_t)(R * QR_NB * 8 * 8));
+  }
+  cluster.sync();   // mbarriers initialised cluster-wide before any remote store
+  for (int idx = t; idx < QR_NB * QR_NB; idx += IBT) {
+    const int i = idx & (QR_NB - 1), j = idx / QR_NB;
+    s_T[idx] = (i < wi && j < wi) ? p.T[i + j * wi] : 0.0;
+  }
+  // W partial: warp (mt, kh) = reflector columns 8 mt.., half kh of the rows
+  {
+    const int mt = warp & 3, kh = warp >> 2;
+    const int64_t nrows = rend - rbeg, hmid = rbeg + (((nrows + 1) / 2 + 3) & ~(int64_t)3);
+    const int64_t lo = kh == 0 ? rbeg : min(hmid, rend), hi = kh == 0 ? min(hmid, rend) : rend;
+    const int mc = mt * 8 + (lane >> 2), nc = lane >> 2;
+    const bool mok = mc < wi, nok = nc < ncol;
+    const double* pv = p.V + (int64_t)mc * p.ldv + (lane & 3);
+    const double* pa = p.A + (int64_t)(n0 + nc) * p.lda + (lane & 3);
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int64_t k0 = lo; k0 < hi; k0 += 32) {
+      double av[8], bv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t kk = k0 + 4 * u + (lane & 3);
+        const bool in = kk < hi;
+        av[u] = (in && mok) ? pv[k0 + 4 * u] : 0.0;
+        bv[u] = (in && nok) ? pa[k0 + 4 * u] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dmma884(acc[u & 1], av[u], bv[u]);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      s_part[kh][(mt * 8 + (lane >> 2)) * 8 + 2 * (lane & 3) + e] = acc[0][e] + acc[1][e];
+  }
+  __syncthreads();
+  {
+    const double wsum = s_part[0][t] + s_part[1][t];
+    const uint32_t dst = smem_addr(&s_all[q][t]);
+    for (int rk = 0; rk < R; ++rk)
+      asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                   ::"r"(cluster_addr(dst, rk)), "l"(__double_as_longlong(wsum)),
+                   "r"(cluster_addr(mb, rk)) : "memory");
+  }
+  mbar_wait(mb, 0);
+  {
+    double tot = 0.0;
+    for (int rk = 0; rk < R; ++rk) tot += s_all[rk][t];
+    s_W[t] = tot;
+  }
+  __syncthreads();
+  {   // W2 = T^T W
+    const int j = t >> 3, n = t & 7;
+    double a0 = 0.0, a1 = 0.0;
+    for (int i = 0; i < QR_NB; i += 2) {
+      a0 = fma(s_T[i + j * QR_NB], s_W[i * 8 + n], a0);
+      a1 = fma(s_T[i + 1 + j * QR_NB], s_W[(i + 1) * 8 + n], a1);
+    }
+    s_W2[t] = a0 + a1;
+  }
+  __syncthreads();
+  // A_r -= V W2 on this CTA's rows, 8-row tiles per warp
+  {
+    const int m = lane >> 2, kq = lane & 3;
+    double bw[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bw[u] = s_W2[(4 * u + kq) * 8 + m];   // B[k][n = m]
+    for (int64_t rt = rbeg + 8 * warp; rt < rend; rt += 8 * (IBT / 32)) {
+      const int64_t row = rt + m;
+      const bool rok = row < rend;
+      double av[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        av[u] = (rok && 4 * u + kq < wi) ? p.V[row + (int64_t)(4 * u + kq) * p.ldv] : 0.0;
+      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dmma884(acc[u & 1], av[u], bw[u]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = 2 * kq + e;
+        if (rok && n < ncol) p.A[row + (int64_t)(n0 + n) * p.lda] -= acc[0][e] + acc[1][e];
+      }
+    }
+  }
+}
+
 __global__ void extract_r_kernel(int64_t k, int64_t n, const double* A, int64_t lda, double* R,
                                  int64_t ldr) {
   const int64_t total = k * n;
@@ -763,6 +883,31 @@ static void factor_panel(cudaStream_t st, double* A, int64_t lda, int64_t mp, in
   note_launch();
 }
 
+// A_r (mp x rem) <- A_r - V T^T (V^T A_r) for one inner panel's reflectors
+// (V mp x wi, T wi x wi), one clustered launch (qr_inblock_cluster_kernel)
+static void inblock_apply(cudaStream_t st, const double* V, int64_t ldv, const double* T, int wi,
+                          double* A, int64_t lda, int64_t mp, int64_t rem) {
+  const int64_t rows = cdiv(cdiv(mp, (int64_t)8), (int64_t)8) * 8;   // <= 8 CTAs along the rows
+  const int64_t rpc = std::max<int64_t>(128, rows);
+  const int R = (int)cdiv(mp, rpc);
+  const int nslab = (int)cdiv(rem, (int64_t)8);
+  InblockArgs a{V, ldv, T, wi, A, lda, mp, (int)rem, (int)rpc};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(R * nslab);
+  cfg.blockDim = dim3(IBT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = R;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, qr_inblock_cluster_kernel, a));
+  note_launch();
+}
+
 // Two-level blocked Householder QR: panels of QR_NB = 32 columns are
 // factored inside outer blocks of NBO = 128 columns; the panel's reflectors
 // update only the rest of their outer block, and the trailing matrix is
@@ -850,10 +995,17 @@ static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A
       if (rem > 0) {
         double* Ar = A + jj + (jj + wi) * lda;
         const double* Vi = Vo + i0 + i0 * mp;
-        ensure(wi * rem);
-        dgemm(ps, true, false, wi, rem, mpi, 1.0, Vi, mp, Ar, lda, 0.0, W.get(), wi);
-        dgemm(ps, true, false, wi, rem, wi, 1.0, Tpi, wi, W.get(), wi, 0.0, W2.get(), wi);
-        dgemm(ps, false, false, mpi, rem, wi, -1.0, Vi, mp, W2.get(), wi, 1.0, Ar, lda);
+        static const bool fused_inblock = std::getenv("MPO_B200_QR_INBLOCK")
+                                              ? std::atoi(std::getenv("MPO_B200_QR_INBLOCK")) != 0
+                                              : true;
+        if (fused_inblock && wi <= QR_NB) {
+          inblock_apply(ps, Vi, mp, Tpi, (int)wi, Ar, lda, mpi, rem);
+        } else {
+          ensure(wi * rem);
+          dgemm(ps, true, false, wi, rem, mpi, 1.0, Vi, mp, Ar, lda, 0.0, W.get(), wi);
+          dgemm(ps, true, false, wi, rem, wi, 1.0, Tpi, wi, W.get(), wi, 0.0, W2.get(), wi);
+          dgemm(ps, false, false, mpi, rem, wi, -1.0, Vi, mp, W2.get(), wi, 1.0, Ar, lda);
+        }
       }
     }
     // trailing update of columns j0+wo .. n-1 with the outer block:
