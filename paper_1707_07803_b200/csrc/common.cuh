@@ -73,6 +73,7 @@ class DBuf {
   T* get() const { return p_; }
   size_t size() const { return n_; }
   cudaStream_t stream() const { return s_; }
+  void set_stream(cudaStream_t s) { s_ = s; }   // the stream the free is ordered on
 
  private:
   T* p_ = nullptr;

@@ -475,6 +475,9 @@ SideStream& side_stream(cudaStream_t main) {
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   CK(cudaStreamCreateWithPriority(&x.hp, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&x.aux, cudaStreamNonBlocking, hi));
+  CK(cudaStreamCreateWithFlags(&x.qs, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&x.eqf, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&x.eq, cudaEventDisableTiming));
   for (auto& e : x.e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   cache.push_back(x);
   return cache.back();

@@ -63,8 +63,19 @@ void core_product(cudaStream_t st, const CoreView& a, const CoreView& b, double*
 // Householder QR of a column-major m x n matrix (qr.cu): on return A holds
 // R in its upper triangle (k = min(m, n) rows) and Q (m x k) is written
 // explicitly; replaces np.linalg.qr(mode="reduced") (LAPACK dgeqrf+dorgqr).
+// defer_q: the explicit Q (dorgqr) is formed on a separate stream after the
+// factorisation, overlapping whatever the caller issues next on st (R is
+// ready in stream order as usual); the caller must join_deferred_q(st) before
+// anything on st reads or frees Q.
 void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda, double* Q,
-                    int64_t ldq, double* R, int64_t ldr);
+                    int64_t ldq, double* R, int64_t ldr, bool defer_q = false);
+void join_deferred_q(cudaStream_t st);
+// joins on scope exit (also when an exception unwinds past pending Q's)
+struct DeferredQScope {
+  cudaStream_t st;
+  explicit DeferredQScope(cudaStream_t s) : st(s) {}
+  ~DeferredQScope() { join_deferred_q(st); }
+};
 // The same factorisation keeping the compact-WY reflectors (no explicit Q),
 // and C <- Q C for an m x ncols matrix C (qr.cu).
 struct QrReflectors {
@@ -145,6 +156,9 @@ struct SideStream {
   int device = -1;
   cudaStream_t hp = nullptr;   // highest-priority stream (latency-critical chains)
   cudaStream_t aux = nullptr;  // highest-priority helper (QR: compact-WY T assembly)
+  cudaStream_t qs = nullptr;   // deferred explicit-Q formation (householder_qr defer_q)
+  cudaEvent_t eqf = nullptr, eq = nullptr;   // factorisation done / Q formed
+  bool q_pending = false;
   cudaEvent_t e[8] = {};
 };
 SideStream& side_stream(cudaStream_t main);

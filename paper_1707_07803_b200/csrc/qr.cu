@@ -916,7 +916,7 @@ static void inblock_apply(cudaStream_t st, const double* V, int64_t ldv, const d
 // from the panels' T's: T = [[T1, -T1 (V1^T V2) T2], [0, T2]].
 static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda,
                                 double* Q, int64_t ldq, double* R, int64_t ldr,
-                                QrReflectors* keep) {
+                                QrReflectors* keep, bool defer_q = false) {
   constexpr int NBO = QrReflectors::NBO;
   const int64_t k = std::min(m, n);
   if (k <= 0) return;
@@ -1064,23 +1064,55 @@ static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A
   if (!Q) return;
   // dorgqr: Q = H_1 ... H_k [I; 0], outer blocks applied last to first (a
   // block's reflectors act only on rows j0.. and, for [I; 0], on columns j0..)
-  set_identity(st, m, k, Q, ldq);
+  cudaStream_t qst = st;
+  SideStream* sq = nullptr;
+  static const bool defer_env = std::getenv("MPO_B200_QR_DEFERQ")
+                                    ? std::atoi(std::getenv("MPO_B200_QR_DEFERQ")) != 0
+                                    : true;
+  if (defer_q && defer_env && !keep) {
+    // on the Q stream, behind the factorisation; V and T are released there
+    sq = &side_stream(st);
+    CK(cudaEventRecord(sq->eqf, st));
+    CK(cudaStreamWaitEvent(sq->qs, sq->eqf, 0));
+    qst = sq->qs;
+    V.set_stream(qst);
+    T.set_stream(qst);
+  }
+  DBuf<double> Wq, Wq2;
+  if (sq) {
+    Wq.alloc((size_t)NBO * k, qst);
+    Wq2.alloc((size_t)NBO * k, qst);
+  }
+  set_identity(qst, m, k, Q, ldq);
   for (int64_t b = nob - 1; b >= 0; --b) {
     const int64_t j0 = b * NBO, wo = wos[b], mp = m - j0, nq = k - j0;
     const double* Vo = (keep ? keep->V.get() : V.get()) + voff[b];
     const double* To = (keep ? keep->T.get() : T.get()) + b * NBO * NBO;
     double* Qb = Q + j0 + j0 * ldq;
-    ensure(wo * nq);
-    dgemm(st, true, false, wo, nq, mp, 1.0, Vo, mp, Qb, ldq, 0.0, W.get(), wo);
-    dgemm(st, false, false, wo, nq, wo, 1.0, To, wo, W.get(), wo, 0.0, W2.get(), wo);
-    dgemm(st, false, false, mp, nq, wo, -1.0, Vo, mp, W2.get(), wo, 1.0, Qb, ldq);
+    if (!sq) ensure(wo * nq);
+    double* w1 = sq ? Wq.get() : W.get();
+    double* w2 = sq ? Wq2.get() : W2.get();
+    dgemm(qst, true, false, wo, nq, mp, 1.0, Vo, mp, Qb, ldq, 0.0, w1, wo);
+    dgemm(qst, false, false, wo, nq, wo, 1.0, To, wo, w1, wo, 0.0, w2, wo);
+    dgemm(qst, false, false, mp, nq, wo, -1.0, Vo, mp, w2, wo, 1.0, Qb, ldq);
+  }
+  if (sq) {
+    CK(cudaEventRecord(sq->eq, qst));
+    sq->q_pending = true;
   }
 }
 
+void join_deferred_q(cudaStream_t st) {
+  SideStream& sd = side_stream(st);
+  if (!sd.q_pending) return;
+  cudaStreamWaitEvent(st, sd.eq, 0);   // no throw: also runs from destructors
+  sd.q_pending = false;
+}
+
 void householder_qr(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda, double* Q,
-                    int64_t ldq, double* R, int64_t ldr) {
+                    int64_t ldq, double* R, int64_t ldr, bool defer_q) {
   if (small_qr(st, m, n, A, lda, Q, ldq, R, ldr)) return;   // one CTA (small.cu)
-  householder_qr_impl(st, m, n, A, lda, Q, ldq, R, ldr, nullptr);
+  householder_qr_impl(st, m, n, A, lda, Q, ldq, R, ldr, nullptr, defer_q);
 }
 
 void householder_qr_keep(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda,

@@ -309,7 +309,10 @@ Cores orthogonalize_product(cudaStream_t st, const Cores* a, bool ta, const Core
     meet = j - 1;
   }
 
-  // 2. L2R QR sweep; the meeting core absorbs Lt on its right
+  // 2. L2R QR sweep; the meeting core absorbs Lt on its right.  The explicit
+  // Q of each step is only read after the sweep: it is formed on the Q stream
+  // while the next step's absorb and latency-bound panels run (joined on exit).
+  DeferredQScope qscope(st);
   DBuf<double> C;   // carried R (m x R_k)
   int64_t m = 1;
   for (size_t k = 0; k < d; ++k) {
@@ -373,7 +376,7 @@ Cores orthogonalize_product(cudaStream_t st, const Cores* a, bool ta, const Core
     DBuf<double> rm((size_t)(kk * cols), st);
     {
       Trace tr(st, "l2r_qr", rows, cols);
-      householder_qr(st, rows, cols, n.p(), rows, q.p(), rows, rm.get(), kk);
+      householder_qr(st, rows, cols, n.p(), rows, q.p(), rows, rm.get(), kk, /*defer_q=*/true);
     }
     out[k] = std::move(q);
     C = std::move(rm);

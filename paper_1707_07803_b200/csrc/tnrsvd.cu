@@ -206,6 +206,7 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
       const bool square = R == N;
       DBuf<double> At((size_t)N * R, st), Qt, Rt((size_t)R * R, st);
       QrReflectors f;
+      DeferredQScope qscope(st);   // joined before Qt is released, also when unwinding
       {
         Trace tr(st, "lq", R, N);
         int64_t dims[2] = {R, N};
@@ -214,8 +215,9 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         if (square) {
           householder_qr_keep(st, N, R, At.get(), N, Rt.get(), R, f);
         } else {
+          // Q' forms on the Q stream while the certificate below runs
           Qt.alloc((size_t)N * R, st);
-          householder_qr(st, N, R, At.get(), N, Qt.get(), N, Rt.get(), R);
+          householder_qr(st, N, R, At.get(), N, Qt.get(), N, Rt.get(), R, /*defer_q=*/true);
         }
       }
       double lb;
@@ -236,6 +238,7 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         fprintf(stderr, "[mpo_b200]   cert R=%lld N=%lld lb/delta=%.3g kappaF=%.3g\n", (long long)R,
                 (long long)N, lb / delta, hr * hi);
       }
+      join_deferred_q(st);
       if (lb > cert_margin * delta) {
         Core nc = make_core(st, R, c.I, c.J, c.S);
         Core np_ = make_core(st, pv.R, pv.I, pv.J, R);
