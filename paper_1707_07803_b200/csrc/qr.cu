@@ -501,45 +501,13 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
       // last block and cluster rank 0's first) take a predicate-free path:
       // the pass is bound by instruction issue, not by shared-memory bandwidth.
       const int ir0 = (int)r0;
-      for (int rb = lane + 32 * half; rb < nr; rb += 64 * QRC_H) {
-        const int rbase = rb - lane;
-        if (refl && ir0 + rbase > pv && rbase + 32 * QRC_H + 32 <= nr) {
-          double x[2], yo[2], a[2][4];
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const int r = rb + 32 * QRC_H * k;
-            x[k] = xj[r];
-            yo[k] = yp[r];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) a[k][u] = cp[u][r];
-          }
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const int r = rb + 32 * QRC_H * k;
-            const double v = x[k] * scal;
-            const double y = fma(-v, wp, yo[k]);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) a[k][u] = fma(-v, wu[u], a[k][u]);
-            if (g0) {
-              a[k][0] = y;
-              ynew[r] = y;
-              xhome[r] = x[k];
-            } else {
-              cp[0][r] = a[k][0];
-            }
-            if (nu > 1) cp[1][r] = a[k][1];
-            if (nu > 2) cp[2][r] = a[k][2];
-            if (nu > 3) cp[3][r] = a[k][3];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] = fma(y, a[k][u], acc[u]);
-          }
-          continue;
-        }
+      constexpr int RS = 32 * QRC_H;        // row stride between a warp's blocks
+      auto slow_trip = [&](int rb) {
         double x[2], yo[2], a[2][4];
         bool live[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          const int r = rb + 32 * QRC_H * k;
+          const int r = rb + RS * k;
           live[k] = r < nr;
           const int rr = live[k] ? r : rb;
           x[k] = refl ? xj[rr] : 0.0;
@@ -549,7 +517,7 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
         }
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          const int r = rb + 32 * QRC_H * k;
+          const int r = rb + RS * k;
           const int gr = ir0 + r;
           if (!live[k]) continue;
           if (gr < jj) {
@@ -577,7 +545,46 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
             for (int u = 0; u < 4; ++u) acc[u] = fma(y, a[k][u], acc[u]);
           }
         }
+      };
+      int rb = lane + 32 * half;
+      // leading trips that touch rows <= pv (cluster rank 0 only)
+      for (; rb < nr && ir0 + (rb - lane) <= pv; rb += 2 * RS) slow_trip(rb);
+      if (refl) {
+        // full blocks entirely below row pv: running pointers, no predicates
+        const double* px = xj + rb;
+        const double* py = yp + rb;
+        double *p0 = cp[0] + rb, *p1 = cp[1] + rb, *p2 = cp[2] + rb, *p3 = cp[3] + rb;
+        double *pyn = ynew + rb, *pxh = xhome + rb;
+        const double nscal = -scal;
+        for (; (rb - lane) + RS + 32 <= nr; rb += 2 * RS) {
+          const double x0 = px[0], x1 = px[RS], y0 = py[0], y1 = py[RS];
+          double a00 = p0[0], a01 = p1[0], a02 = p2[0], a03 = p3[0];
+          double a10 = p0[RS], a11 = p1[RS], a12 = p2[RS], a13 = p3[RS];
+          const double v0 = x0 * nscal, v1 = x1 * nscal;   // -v
+          const double yy0 = fma(v0, wp, y0), yy1 = fma(v1, wp, y1);
+          a00 = fma(v0, wu[0], a00); a01 = fma(v0, wu[1], a01);
+          a02 = fma(v0, wu[2], a02); a03 = fma(v0, wu[3], a03);
+          a10 = fma(v1, wu[0], a10); a11 = fma(v1, wu[1], a11);
+          a12 = fma(v1, wu[2], a12); a13 = fma(v1, wu[3], a13);
+          if (g0) {
+            a00 = yy0; a10 = yy1;
+            pyn[0] = yy0; pyn[RS] = yy1;
+            pxh[0] = x0; pxh[RS] = x1;
+          } else {
+            p0[0] = a00; p0[RS] = a10;
+          }
+          if (nu > 1) { p1[0] = a01; p1[RS] = a11; }
+          if (nu > 2) { p2[0] = a02; p2[RS] = a12; }
+          if (nu > 3) { p3[0] = a03; p3[RS] = a13; }
+          acc[0] = fma(yy0, a00, acc[0]); acc[1] = fma(yy0, a01, acc[1]);
+          acc[2] = fma(yy0, a02, acc[2]); acc[3] = fma(yy0, a03, acc[3]);
+          acc[0] = fma(yy1, a10, acc[0]); acc[1] = fma(yy1, a11, acc[1]);
+          acc[2] = fma(yy1, a12, acc[2]); acc[3] = fma(yy1, a13, acc[3]);
+          px += 2 * RS; py += 2 * RS; p0 += 2 * RS; p1 += 2 * RS; p2 += 2 * RS; p3 += 2 * RS;
+          pyn += 2 * RS; pxh += 2 * RS;
+        }
       }
+      for (; rb < nr; rb += 2 * RS) slow_trip(rb);
       // transposing butterfly: 4 sums over 32 lanes in 6 exchanges; lane
       // 8u ends with column col0 + u
       const bool hi = lane & 16, mid = lane & 8;
