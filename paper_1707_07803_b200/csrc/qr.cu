@@ -667,13 +667,14 @@ struct InblockArgs {
   int rem;
   int rpc;           // rows per CTA
 };
-constexpr int IBT = 256;
+constexpr int IBT = 512;          // 16 warps: 4 reflector-column tiles x 4 row quarters
+constexpr int IB_MAXR = 16;       // cluster size along the rows (non-portable above 8)
 __global__ void __launch_bounds__(IBT) qr_inblock_cluster_kernel(InblockArgs p) {
-  __shared__ double s_part[2][QR_NB * 8];
-  __shared__ double s_all[8][QR_NB * 8];
+  __shared__ double s_part[4][QR_NB * 8];   // row-quarter partials, then T (same size)
+  __shared__ double s_all[IB_MAXR][QR_NB * 8];
   __shared__ double s_W[QR_NB * 8], s_W2[QR_NB * 8];
-  __shared__ double s_T[QR_NB * QR_NB];
   __shared__ __align__(8) unsigned long long s_mbar;
+  double* s_T = &s_part[0][0];
   cg::cluster_group cluster = cg::this_cluster();
   const int R = (int)cluster.num_blocks(), q = (int)cluster.block_rank();
   const int slab = blockIdx.x / R;
@@ -687,15 +688,11 @@ __global__ void __launch_bounds__(IBT) qr_inblock_cluster_kernel(InblockArgs p) 
     mbar_expect_tx(mb, (uint32_t)(R * QR_NB * 8 * 8));
   }
   cluster.sync();   // mbarriers initialised cluster-wide before any remote store
-  for (int idx = t; idx < QR_NB * QR_NB; idx += IBT) {
-    const int i = idx & (QR_NB - 1), j = idx / QR_NB;
-    s_T[idx] = (i < wi && j < wi) ? p.T[i + j * wi] : 0.0;
-  }
-  // W partial: warp (mt, kh) = reflector columns 8 mt.., half kh of the rows
+  // W partial: warp (mt, kq) = reflector columns 8 mt.., quarter kq of the rows
   {
-    const int mt = warp & 3, kh = warp >> 2;
-    const int64_t nrows = rend - rbeg, hmid = rbeg + (((nrows + 1) / 2 + 3) & ~(int64_t)3);
-    const int64_t lo = kh == 0 ? rbeg : min(hmid, rend), hi = kh == 0 ? min(hmid, rend) : rend;
+    const int mt = warp & 3, kq = warp >> 2;
+    const int64_t nrows = rend - rbeg, qlen = (((nrows + 3) / 4 + 3) & ~(int64_t)3);
+    const int64_t lo = min(rbeg + kq * qlen, rend), hi = min(lo + qlen, rend);
     const int mc = mt * 8 + (lane >> 2), nc = lane >> 2;
     const bool mok = mc < wi, nok = nc < ncol;
     const double* pv = p.V + (int64_t)mc * p.ldv + (lane & 3);
@@ -715,25 +712,30 @@ __global__ void __launch_bounds__(IBT) qr_inblock_cluster_kernel(InblockArgs p) 
     }
 #pragma unroll
     for (int e = 0; e < 2; ++e)
-      s_part[kh][(mt * 8 + (lane >> 2)) * 8 + 2 * (lane & 3) + e] = acc[0][e] + acc[1][e];
+      s_part[kq][(mt * 8 + (lane >> 2)) * 8 + 2 * (lane & 3) + e] = acc[0][e] + acc[1][e];
   }
   __syncthreads();
-  {
-    const double wsum = s_part[0][t] + s_part[1][t];
+  if (t < QR_NB * 8) {
+    const double wsum = (s_part[0][t] + s_part[1][t]) + (s_part[2][t] + s_part[3][t]);
     const uint32_t dst = smem_addr(&s_all[q][t]);
     for (int rk = 0; rk < R; ++rk)
       asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
                    ::"r"(cluster_addr(dst, rk)), "l"(__double_as_longlong(wsum)),
                    "r"(cluster_addr(mb, rk)) : "memory");
   }
+  __syncthreads();   // the partials are consumed: their buffer takes T
+  for (int idx = t; idx < QR_NB * QR_NB; idx += IBT) {
+    const int i = idx & (QR_NB - 1), j = idx / QR_NB;
+    s_T[idx] = (i < wi && j < wi) ? p.T[i + j * wi] : 0.0;
+  }
   mbar_wait(mb, 0);
-  {
+  if (t < QR_NB * 8) {
     double tot = 0.0;
     for (int rk = 0; rk < R; ++rk) tot += s_all[rk][t];
     s_W[t] = tot;
   }
   __syncthreads();
-  {   // W2 = T^T W
+  if (t < QR_NB * 8) {   // W2 = T^T W
     const int j = t >> 3, n = t & 7;
     double a0 = 0.0, a1 = 0.0;
     for (int i = 0; i < QR_NB; i += 2) {
@@ -756,13 +758,17 @@ __global__ void __launch_bounds__(IBT) qr_inblock_cluster_kernel(InblockArgs p) 
 #pragma unroll
       for (int u = 0; u < 8; ++u)
         av[u] = (rok && 4 * u + kq < wi) ? p.V[row + (int64_t)(4 * u + kq) * p.ldv] : 0.0;
+      double cold[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        cold[e] = (rok && 2 * kq + e < ncol) ? p.A[row + (int64_t)(n0 + 2 * kq + e) * p.lda] : 0.0;
       double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
       for (int u = 0; u < 8; ++u) dmma884(acc[u & 1], av[u], bw[u]);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int n = 2 * kq + e;
-        if (rok && n < ncol) p.A[row + (int64_t)(n0 + n) * p.lda] -= acc[0][e] + acc[1][e];
+        if (rok && n < ncol) p.A[row + (int64_t)(n0 + n) * p.lda] = cold[e] - (acc[0][e] + acc[1][e]);
       }
     }
   }
@@ -894,7 +900,14 @@ static void factor_panel(cudaStream_t st, double* A, int64_t lda, int64_t mp, in
 // (V mp x wi, T wi x wi), one clustered launch (qr_inblock_cluster_kernel)
 static void inblock_apply(cudaStream_t st, const double* V, int64_t ldv, const double* T, int wi,
                           double* A, int64_t lda, int64_t mp, int64_t rem) {
-  const int64_t rows = cdiv(cdiv(mp, (int64_t)8), (int64_t)8) * 8;   // <= 8 CTAs along the rows
+  // <= 8 CTAs along the rows, 16 for tall panels (512-row slices)
+  static std::once_flag once[kMaxDevices];
+  once_per_device(once, [] {
+    CK(cudaFuncSetAttribute(qr_inblock_cluster_kernel,
+                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
+  const int maxr = mp > 4096 ? IB_MAXR : 8;
+  const int64_t rows = cdiv(cdiv(mp, (int64_t)maxr), (int64_t)8) * 8;
   const int64_t rpc = std::max<int64_t>(128, rows);
   const int R = (int)cdiv(mp, rpc);
   const int nslab = (int)cdiv(rem, (int64_t)8);
