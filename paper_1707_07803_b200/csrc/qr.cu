@@ -648,129 +648,149 @@ __global__ void __launch_bounds__(QRC) qr_panel_cluster_kernel(ClusterPanelArgs 
 #endif
 }
 
-// In-block update of a panel's reflectors on the rest of their outer block,
-// A_r <- (I - V T V^T)^T A_r = A_r - V T^T (V^T A_r), in ONE launch instead of
-// three skinny GEMMs (K = panel height for an output of 32 x <= 96: 7-13 us
-// each on the panel chain).  Column slabs of 8 x clusters of R CTAs along the
-// rows: a CTA forms its rows' part of W = V^T A_r (32 x 8, DMMA, fragments
-// straight from L2), the cluster all-gathers the partials with st.async on
-// each rank's mbarrier (fixed rank-order sum), then every CTA applies
-// A_r -= V (T^T W) to its rows.
+// Application of inner panels' reflectors to a column range in ONE launch:
+//   A_r <- (I - V_i T_i V_i^T)^T A_r = A_r - V_i T_i^T (V_i^T A_r),  i = 0 .. npan-1 in order,
+// instead of three skinny GEMMs per panel (K = panel height for an output of
+// 32 x <= 128: 7-13 us each on the panel chain).  Used for the in-block update
+// (one panel, the rest of its outer block) and for the look-ahead ("near")
+// update of the next outer block's columns with all of a block's panels --
+// which then needs only the panels' own T factors, not the assembled outer T.
+// Column slabs of 8 x clusters of R CTAs along the rows: a CTA forms its rows'
+// part of W = V_i^T A_r (wi x 8, DMMA, fragments straight from L2), the cluster
+// all-gathers the partials with st.async on each rank's mbarrier (fixed
+// rank-order sum; buffers and mbarriers alternate by panel parity), then every
+// CTA applies A_r -= V_i (T_i^T W) to its rows.
+constexpr int IB_MAXP = 16;       // panels per launch (an outer block of 8-column panels)
 struct InblockArgs {
-  const double* V;   // mp x wi, ld ldv (unit diagonal, zeros above)
+  const double* V;   // mp x (sum of widths), ld ldv: unit diagonals, zeros above
   int64_t ldv;
-  const double* T;   // wi x wi upper triangular, ld wi
-  int wi;
+  const double* T;   // panel i's wi x wi upper triangular factor at T + toff[i], ld wi
   double* A;         // mp x rem, ld lda
   int64_t lda;
   int64_t mp;
   int rem;
   int rpc;           // rows per CTA
+  int npan;
+  int voff[IB_MAXP]; // first column of panel i in V
+  int wid[IB_MAXP];  // its width (<= 32)
+  int toff[IB_MAXP];
 };
 constexpr int IBT = 512;          // 16 warps: 4 reflector-column tiles x 4 row quarters
 constexpr int IB_MAXR = 16;       // cluster size along the rows (non-portable above 8)
-__global__ void __launch_bounds__(IBT) qr_inblock_cluster_kernel(InblockArgs p) {
-  __shared__ double s_part[4][QR_NB * 8];   // row-quarter partials, then T (same size)
-  __shared__ double s_all[IB_MAXR][QR_NB * 8];
+constexpr int IB_SMEM = 2 * IB_MAXR * QR_NB * 8 * (int)sizeof(double);
+__global__ void __launch_bounds__(IBT, 2) qr_inblock_cluster_kernel(InblockArgs p) {
+  extern __shared__ double s_all[];        // [2][IB_MAXR][QR_NB * 8] gathered partials, by parity
+  __shared__ double s_part[4][QR_NB * 8];  // row-quarter partials, then T (same size)
   __shared__ double s_W[QR_NB * 8], s_W2[QR_NB * 8];
-  __shared__ __align__(8) unsigned long long s_mbar;
+  __shared__ __align__(8) unsigned long long s_mbar[2];
   double* s_T = &s_part[0][0];
   cg::cluster_group cluster = cg::this_cluster();
   const int R = (int)cluster.num_blocks(), q = (int)cluster.block_rank();
   const int slab = blockIdx.x / R;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int wi = p.wi, n0 = slab * 8, ncol = min(8, p.rem - n0);
+  const int n0 = slab * 8, ncol = min(8, p.rem - n0);
   const int64_t rbeg = (int64_t)q * p.rpc, rend = min(p.mp, rbeg + p.rpc);
-  const uint32_t mb = smem_addr(&s_mbar);
   if (t == 0) {
-    mbar_init(mb, 1);
+    mbar_init(smem_addr(&s_mbar[0]), 1);
+    mbar_init(smem_addr(&s_mbar[1]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(mb, (uint32_t)(R * QR_NB * 8 * 8));
   }
   cluster.sync();   // mbarriers initialised cluster-wide before any remote store
-  // W partial: warp (mt, kq) = reflector columns 8 mt.., quarter kq of the rows
-  {
-    const int mt = warp & 3, kq = warp >> 2;
-    const int64_t nrows = rend - rbeg, qlen = (((nrows + 3) / 4 + 3) & ~(int64_t)3);
-    const int64_t lo = min(rbeg + kq * qlen, rend), hi = min(lo + qlen, rend);
-    const int mc = mt * 8 + (lane >> 2), nc = lane >> 2;
-    const bool mok = mc < wi, nok = nc < ncol;
-    const double* pv = p.V + (int64_t)mc * p.ldv + (lane & 3);
-    const double* pa = p.A + (int64_t)(n0 + nc) * p.lda + (lane & 3);
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    for (int64_t k0 = lo; k0 < hi; k0 += 32) {
-      double av[8], bv[8];
+  for (int ph = 0; ph < p.npan; ++ph) {
+    const int wi = p.wid[ph];
+    const double* Vp = p.V + (int64_t)p.voff[ph] * p.ldv;
+    const uint32_t mb = smem_addr(&s_mbar[ph & 1]);
+    double* all = s_all + (ph & 1) * (IB_MAXR * QR_NB * 8);
+    if (t == 0) mbar_expect_tx(mb, (uint32_t)(R * QR_NB * 8 * 8));
+    // W partial: warp (mt, kq) = reflector columns 8 mt.., quarter kq of the rows
+    {
+      const int mt = warp & 3, kq = warp >> 2;
+      const int64_t nrows = rend - rbeg, qlen = (((nrows + 3) / 4 + 3) & ~(int64_t)3);
+      const int64_t lo = min(rbeg + kq * qlen, rend), hi = min(lo + qlen, rend);
+      const int mc = mt * 8 + (lane >> 2), nc = lane >> 2;
+      const bool mok = mc < wi, nok = nc < ncol;
+      const double* pv = Vp + (int64_t)mc * p.ldv + (lane & 3);
+      const double* pa = p.A + (int64_t)(n0 + nc) * p.lda + (lane & 3);
+      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      if (mt * 8 < wi)
+        for (int64_t k0 = lo; k0 < hi; k0 += 32) {
+          double av[8], bv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t kk = k0 + 4 * u + (lane & 3);
-        const bool in = kk < hi;
-        av[u] = (in && mok) ? pv[k0 + 4 * u] : 0.0;
-        bv[u] = (in && nok) ? pa[k0 + 4 * u] : 0.0;
-      }
+          for (int u = 0; u < 8; ++u) {
+            const int64_t kk = k0 + 4 * u + (lane & 3);
+            const bool in = kk < hi;
+            av[u] = (in && mok) ? pv[k0 + 4 * u] : 0.0;
+            bv[u] = (in && nok) ? pa[k0 + 4 * u] : 0.0;
+          }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) dmma884(acc[u & 1], av[u], bv[u]);
-    }
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-      s_part[kq][(mt * 8 + (lane >> 2)) * 8 + 2 * (lane & 3) + e] = acc[0][e] + acc[1][e];
-  }
-  __syncthreads();
-  if (t < QR_NB * 8) {
-    const double wsum = (s_part[0][t] + s_part[1][t]) + (s_part[2][t] + s_part[3][t]);
-    const uint32_t dst = smem_addr(&s_all[q][t]);
-    for (int rk = 0; rk < R; ++rk)
-      asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
-                   ::"r"(cluster_addr(dst, rk)), "l"(__double_as_longlong(wsum)),
-                   "r"(cluster_addr(mb, rk)) : "memory");
-  }
-  __syncthreads();   // the partials are consumed: their buffer takes T
-  for (int idx = t; idx < QR_NB * QR_NB; idx += IBT) {
-    const int i = idx & (QR_NB - 1), j = idx / QR_NB;
-    s_T[idx] = (i < wi && j < wi) ? p.T[i + j * wi] : 0.0;
-  }
-  mbar_wait(mb, 0);
-  if (t < QR_NB * 8) {
-    double tot = 0.0;
-    for (int rk = 0; rk < R; ++rk) tot += s_all[rk][t];
-    s_W[t] = tot;
-  }
-  __syncthreads();
-  if (t < QR_NB * 8) {   // W2 = T^T W
-    const int j = t >> 3, n = t & 7;
-    double a0 = 0.0, a1 = 0.0;
-    for (int i = 0; i < QR_NB; i += 2) {
-      a0 = fma(s_T[i + j * QR_NB], s_W[i * 8 + n], a0);
-      a1 = fma(s_T[i + 1 + j * QR_NB], s_W[(i + 1) * 8 + n], a1);
-    }
-    s_W2[t] = a0 + a1;
-  }
-  __syncthreads();
-  // A_r -= V W2 on this CTA's rows, 8-row tiles per warp
-  {
-    const int m = lane >> 2, kq = lane & 3;
-    double bw[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) bw[u] = s_W2[(4 * u + kq) * 8 + m];   // B[k][n = m]
-    for (int64_t rt = rbeg + 8 * warp; rt < rend; rt += 8 * (IBT / 32)) {
-      const int64_t row = rt + m;
-      const bool rok = row < rend;
-      double av[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        av[u] = (rok && 4 * u + kq < wi) ? p.V[row + (int64_t)(4 * u + kq) * p.ldv] : 0.0;
-      double cold[2];
+          for (int u = 0; u < 8; ++u) dmma884(acc[u & 1], av[u], bv[u]);
+        }
 #pragma unroll
       for (int e = 0; e < 2; ++e)
-        cold[e] = (rok && 2 * kq + e < ncol) ? p.A[row + (int64_t)(n0 + 2 * kq + e) * p.lda] : 0.0;
-      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-      for (int u = 0; u < 8; ++u) dmma884(acc[u & 1], av[u], bw[u]);
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int n = 2 * kq + e;
-        if (rok && n < ncol) p.A[row + (int64_t)(n0 + n) * p.lda] = cold[e] - (acc[0][e] + acc[1][e]);
+        s_part[kq][(mt * 8 + (lane >> 2)) * 8 + 2 * (lane & 3) + e] = acc[0][e] + acc[1][e];
+    }
+    __syncthreads();
+    if (t < QR_NB * 8) {
+      const double wsum = (s_part[0][t] + s_part[1][t]) + (s_part[2][t] + s_part[3][t]);
+      const uint32_t dst = smem_addr(&all[q * (QR_NB * 8) + t]);
+      for (int rk = 0; rk < R; ++rk)
+        asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                     ::"r"(cluster_addr(dst, rk)), "l"(__double_as_longlong(wsum)),
+                     "r"(cluster_addr(mb, rk)) : "memory");
+    }
+    __syncthreads();   // the partials are consumed: their buffer takes T
+    {
+      const double* Tp = p.T + p.toff[ph];
+      for (int idx = t; idx < QR_NB * QR_NB; idx += IBT) {
+        const int i = idx & (QR_NB - 1), j = idx / QR_NB;
+        s_T[idx] = (i < wi && j < wi) ? Tp[i + j * wi] : 0.0;
       }
     }
+    mbar_wait(mb, (ph >> 1) & 1);
+    if (t < QR_NB * 8) {
+      double tot = 0.0;
+      for (int rk = 0; rk < R; ++rk) tot += all[rk * (QR_NB * 8) + t];
+      s_W[t] = tot;
+    }
+    __syncthreads();
+    if (t < QR_NB * 8) {   // W2 = T^T W
+      const int j = t >> 3, n = t & 7;
+      double a0 = 0.0, a1 = 0.0;
+      for (int i = 0; i < QR_NB; i += 2) {
+        a0 = fma(s_T[i + j * QR_NB], s_W[i * 8 + n], a0);
+        a1 = fma(s_T[i + 1 + j * QR_NB], s_W[(i + 1) * 8 + n], a1);
+      }
+      s_W2[t] = a0 + a1;
+    }
+    __syncthreads();
+    // A_r -= V W2 on this CTA's rows, 8-row tiles per warp
+    {
+      const int m = lane >> 2, kq = lane & 3;
+      double bw[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) bw[u] = s_W2[(4 * u + kq) * 8 + m];   // B[k][n = m]
+      for (int64_t rt = rbeg + 8 * warp; rt < rend; rt += 8 * (IBT / 32)) {
+        const int64_t row = rt + m;
+        const bool rok = row < rend;
+        double av[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          av[u] = (rok && 4 * u + kq < wi) ? Vp[row + (int64_t)(4 * u + kq) * p.ldv] : 0.0;
+        double cold[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          cold[e] = (rok && 2 * kq + e < ncol) ? p.A[row + (int64_t)(n0 + 2 * kq + e) * p.lda] : 0.0;
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dmma884(acc[u & 1], av[u], bw[u]);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = 2 * kq + e;
+          if (rok && n < ncol) p.A[row + (int64_t)(n0 + n) * p.lda] = cold[e] - (acc[0][e] + acc[1][e]);
+        }
+      }
+    }
+    __syncthreads();   // this CTA's rows of A_r are updated before the next panel reads them
   }
 }
 
@@ -896,26 +916,34 @@ static void factor_panel(cudaStream_t st, double* A, int64_t lda, int64_t mp, in
   note_launch();
 }
 
-// A_r (mp x rem) <- A_r - V T^T (V^T A_r) for one inner panel's reflectors
-// (V mp x wi, T wi x wi), one clustered launch (qr_inblock_cluster_kernel)
-static void inblock_apply(cudaStream_t st, const double* V, int64_t ldv, const double* T, int wi,
-                          double* A, int64_t lda, int64_t mp, int64_t rem) {
+// A_r (mp x rem) <- A_r - V_i T_i^T (V_i^T A_r), i = 0 .. npan-1, for panels
+// i of widths wid[i] at columns voff[i] of V (ld ldv, full height mp: zeros
+// above each unit diagonal) with T_i at T + toff[i]; one clustered launch
+// (qr_inblock_cluster_kernel)
+static void panels_apply(cudaStream_t st, const double* V, int64_t ldv, const double* T, int npan,
+                         const int* voff, const int* wid, const int* toff, double* A, int64_t lda,
+                         int64_t mp, int64_t rem) {
   // <= 8 CTAs along the rows, 16 for tall panels (512-row slices)
   static std::once_flag once[kMaxDevices];
   once_per_device(once, [] {
     CK(cudaFuncSetAttribute(qr_inblock_cluster_kernel,
                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaFuncSetAttribute(qr_inblock_cluster_kernel,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, IB_SMEM));
   });
   const int maxr = mp > 4096 ? IB_MAXR : 8;
   const int64_t rows = cdiv(cdiv(mp, (int64_t)maxr), (int64_t)8) * 8;
   const int64_t rpc = std::max<int64_t>(128, rows);
   const int R = (int)cdiv(mp, rpc);
   const int nslab = (int)cdiv(rem, (int64_t)8);
-  InblockArgs a{V, ldv, T, wi, A, lda, mp, (int)rem, (int)rpc};
+  InblockArgs a{};
+  a.V = V; a.ldv = ldv; a.T = T; a.A = A; a.lda = lda; a.mp = mp; a.rem = (int)rem;
+  a.rpc = (int)rpc; a.npan = npan;
+  for (int i = 0; i < npan; ++i) { a.voff[i] = voff[i]; a.wid[i] = wid[i]; a.toff[i] = toff[i]; }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(R * nslab);
   cfg.blockDim = dim3(IBT);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = IB_SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -988,14 +1016,28 @@ static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A
     Ws.alloc((size_t)NBO * n, sd->sv);
     Ws2.alloc((size_t)NBO * n, sd->sv);
   }
+  static const bool fused_inblock = std::getenv("MPO_B200_QR_INBLOCK")
+                                        ? std::atoi(std::getenv("MPO_B200_QR_INBLOCK")) != 0
+                                        : true;
+  static const bool fused_near = std::getenv("MPO_B200_QR_NEAR")
+                                     ? std::atoi(std::getenv("MPO_B200_QR_NEAR")) != 0
+                                     : true;
   for (int64_t b = 0; b < nob; ++b) {
     const int64_t j0 = b * NBO, wo = wos[b], mp = m - j0;
     double* Vo = V.get() + voff[b];
     double* To = T.get() + b * NBO * NBO;   // ld wo
+    int pan_off[IB_MAXP], pan_w[IB_MAXP], pan_t[IB_MAXP], npan = 0;   // this block's panels
+    bool pan_ok = true;
     for (int64_t i0 = 0, wi = 0; i0 < wo; i0 += wi) {
       const int64_t jj = j0 + i0, mpi = m - jj;
       wi = std::min<int64_t>(panel_width(mpi, QR_NB), wo - i0);
       double* Tpi = TpAll.get() + i0 * QR_NB * QR_NB;
+      if (npan < IB_MAXP && wi <= QR_NB) {
+        pan_off[npan] = (int)i0; pan_w[npan] = (int)wi; pan_t[npan] = (int)(i0 * QR_NB * QR_NB);
+        ++npan;
+      } else {
+        pan_ok = false;
+      }
       factor_panel(ps, A + jj + jj * lda, lda, mpi, wi, Vo + i0 + i0 * mp, mp, Tpi,
                    tau.get() + jj, part.get(), wpart.get(), vtv.get(), alpha.get());
       if (la) {
@@ -1015,11 +1057,9 @@ static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A
       if (rem > 0) {
         double* Ar = A + jj + (jj + wi) * lda;
         const double* Vi = Vo + i0 + i0 * mp;
-        static const bool fused_inblock = std::getenv("MPO_B200_QR_INBLOCK")
-                                              ? std::atoi(std::getenv("MPO_B200_QR_INBLOCK")) != 0
-                                              : true;
         if (fused_inblock && wi <= QR_NB) {
-          inblock_apply(ps, Vi, mp, Tpi, (int)wi, Ar, lda, mpi, rem);
+          const int z = 0, wv = (int)wi;
+          panels_apply(ps, Vi, mp, Tpi, 1, &z, &wv, &z, Ar, lda, mpi, rem);
         } else {
           ensure(wi * rem);
           dgemm(ps, true, false, wi, rem, mpi, 1.0, Vi, mp, Ar, lda, 0.0, W.get(), wi);
@@ -1034,26 +1074,34 @@ static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A
     // stream and overlap the next block's latency-bound panels (<= 16 SMs).
     // Main waits for far(b-1) before near(b): the near columns were part of
     // far(b-1)'s range.
-    if (la) {   // the outer T of this block is assembled
-      CK(cudaEventRecord(ev_t, ts));
-      CK(cudaStreamWaitEvent(ps, ev_t, 0));
-    }
+    if (la) CK(cudaEventRecord(ev_t, ts));   // the outer T of this block is assembled
     const int64_t nt = n - (j0 + wo);
+    const int64_t near = nt <= 0 ? 0 : (la ? std::min<int64_t>(nt, NBO) : nt), far = nt - near;
+    // near update straight from the panels' own (V_i, T_i), one launch: the
+    // panel chain does not wait for the assembled outer T
+    const bool near_fused = fused_inblock && fused_near && pan_ok && near > 0 && near <= NBO;
+    if (la && !(nt > 0 && near_fused)) CK(cudaStreamWaitEvent(ps, ev_t, 0));
     if (nt > 0) {
-      const int64_t near = la ? std::min<int64_t>(nt, NBO) : nt, far = nt - near;
       double* At = A + j0 + (j0 + wo) * lda;
       if (la) {
-        CK(cudaEventRecord(ev_panel, ps));   // block b's V, T are ready
+        CK(cudaEventRecord(ev_panel, ps));   // block b's V is ready
         if (b > 0) CK(cudaStreamWaitEvent(ps, ev_far, 0));
       }
-      ensure(wo * near);
-      dgemm(ps, true, false, wo, near, mp, 1.0, Vo, mp, At, lda, 0.0, W.get(), wo);
-      dgemm(ps, true, false, wo, near, wo, 1.0, To, wo, W.get(), wo, 0.0, W2.get(), wo);
-      dgemm(ps, false, false, mp, near, wo, -1.0, Vo, mp, W2.get(), wo, 1.0, At, lda);
+      if (near_fused) {
+        panels_apply(ps, Vo, mp, TpAll.get(), npan, pan_off, pan_w, pan_t, At, lda, mp, near);
+        // the next block's panels overwrite the T slots the assembly reads
+        if (la) CK(cudaStreamWaitEvent(ps, ev_t, 0));
+      } else {
+        ensure(wo * near);
+        dgemm(ps, true, false, wo, near, mp, 1.0, Vo, mp, At, lda, 0.0, W.get(), wo);
+        dgemm(ps, true, false, wo, near, wo, 1.0, To, wo, W.get(), wo, 0.0, W2.get(), wo);
+        dgemm(ps, false, false, mp, near, wo, -1.0, Vo, mp, W2.get(), wo, 1.0, At, lda);
+      }
       if (far > 0) {
         cudaStream_t sv = sd->sv;
         double* Af = At + near * lda;
         CK(cudaStreamWaitEvent(sv, ev_panel, 0));
+        CK(cudaStreamWaitEvent(sv, ev_t, 0));
         dgemm(sv, true, false, wo, far, mp, 1.0, Vo, mp, Af, lda, 0.0, Ws.get(), wo);
         dgemm(sv, true, false, wo, far, wo, 1.0, To, wo, Ws.get(), wo, 0.0, Ws2.get(), wo);
         dgemm(sv, false, false, mp, far, wo, -1.0, Vo, mp, Ws2.get(), wo, 1.0, Af, lda);
