@@ -386,7 +386,7 @@ def run_b200(args, rank, world, local_rank):
     prof = {}
     import ctypes as C
     names = ["jacobi_gram_kernel", "jacobi_eig_kernel", "jacobi_apply_kernel", "dgemm_kernel",
-             "qr_panel_cluster_kernel"]
+             "qr_panel_cluster_kernel", "qr_inblock_cluster_kernel"]
     for idx, kname in enumerate(names):
         ms, fl, n = C.c_double(), C.c_double(), C.c_ulonglong()
         _lib.call("mpo_b200_profile_read", idx, C.byref(ms), C.byref(fl), C.byref(n))

@@ -9,10 +9,11 @@ namespace mpob {
 
 // Optional per-kernel CUDA-event timing (bench.py's roofline): 0 =
 // jacobi_gram, 1 = jacobi_eig, 2 = jacobi_apply, 3 = dgemm (+ its split-K
-// reduction), 4 = QR panel.  Each timed launch synchronises its stream
-// (profiling runs only).
+// reduction), 4 = QR panel, 5 = QR panel-reflector application (in-block /
+// look-ahead update).  Each timed launch synchronises its stream (profiling
+// runs only).
 struct KernelProfile {
-  static constexpr int N = 5;
+  static constexpr int N = 6;
   bool on = false;
   double ms[N] = {};
   double flops[N] = {};
