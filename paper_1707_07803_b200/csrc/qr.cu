@@ -1025,6 +1025,9 @@ static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A
   static const bool fused_inblock = std::getenv("MPO_B200_QR_INBLOCK")
                                         ? std::atoi(std::getenv("MPO_B200_QR_INBLOCK")) != 0
                                         : true;
+  // taller panels leave > 1024 rows to each CTA of a 16-CTA row cluster: the
+  // split-K GEMMs over all SMs are faster there (row-sharded TSQR's local QRs)
+  constexpr int64_t kFusedApplyMaxRows = 16384;
   static const bool fused_near = std::getenv("MPO_B200_QR_NEAR")
                                      ? std::atoi(std::getenv("MPO_B200_QR_NEAR")) != 0
                                      : true;
@@ -1063,7 +1066,7 @@ static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A
       if (rem > 0) {
         double* Ar = A + jj + (jj + wi) * lda;
         const double* Vi = Vo + i0 + i0 * mp;
-        if (fused_inblock && wi <= QR_NB) {
+        if (fused_inblock && wi <= QR_NB && mpi <= kFusedApplyMaxRows) {
           const int z = 0, wv = (int)wi;
           panels_apply(ps, Vi, mp, Tpi, 1, &z, &wv, &z, Ar, lda, mpi, rem);
         } else {
@@ -1085,7 +1088,8 @@ static void householder_qr_impl(cudaStream_t st, int64_t m, int64_t n, double* A
     const int64_t near = nt <= 0 ? 0 : (la ? std::min<int64_t>(nt, NBO) : nt), far = nt - near;
     // near update straight from the panels' own (V_i, T_i), one launch: the
     // panel chain does not wait for the assembled outer T
-    const bool near_fused = fused_inblock && fused_near && pan_ok && near > 0 && near <= NBO;
+    const bool near_fused = fused_inblock && fused_near && pan_ok && near > 0 && near <= NBO &&
+                            mp <= kFusedApplyMaxRows;
     if (la && !(nt > 0 && near_fused)) CK(cudaStreamWaitEvent(ps, ev_t, 0));
     if (nt > 0) {
       double* At = A + j0 + (j0 + wo) * lda;
