@@ -173,6 +173,38 @@ void l2r(cudaStream_t st, Cores& cores) {
   }
 }
 
+// C (m x k) = A (m x k) * U^T for an upper-triangular U (k x k): column block
+// j of C only needs A's columns from the block on (half the flops of the full
+// product for large k)
+static void gemm_a_ut(cudaStream_t st, int64_t m, int64_t k, const double* A, int64_t lda,
+                      const double* U, int64_t ldu, double* C, int64_t ldc) {
+  const int64_t nb = 512;
+  if (k <= 2 * nb) {
+    dgemm(st, false, true, m, k, k, 1.0, A, lda, U, ldu, 0.0, C, ldc);
+    return;
+  }
+  for (int64_t j0 = 0; j0 < k; j0 += nb) {
+    const int64_t nj = std::min(nb, k - j0);
+    dgemm(st, false, true, m, nj, k - j0, 1.0, A + j0 * lda, lda, U + j0 + j0 * ldu, ldu, 0.0,
+          C + j0 * ldc, ldc);
+  }
+}
+
+// C (k x n) = U^T * B (k x n) for an upper-triangular U (k x k): row block i
+// of C only needs rows 0 .. i0 + mi - 1 of U's column block and of B
+static void gemm_ut_b(cudaStream_t st, int64_t k, int64_t n, const double* U, int64_t ldu,
+                      const double* B, int64_t ldb, double* C, int64_t ldc) {
+  const int64_t nb = 512;
+  if (k <= 2 * nb) {
+    dgemm(st, true, false, k, n, k, 1.0, U, ldu, B, ldb, 0.0, C, ldc);
+    return;
+  }
+  for (int64_t i0 = 0; i0 < k; i0 += nb) {
+    const int64_t mi = std::min(nb, k - i0);
+    dgemm(st, true, false, mi, n, i0 + mi, 1.0, U + i0 * ldu, ldu, B, ldb, 0.0, C + i0, ldc);
+  }
+}
+
 // rsvd.py:111-136, the truncating half: cores are left-orthonormal (after
 // l2r or orthogonalize_product); delta from the last core's norm (:123)
 void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
@@ -251,7 +283,7 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
           int64_t dims[2] = {N, R};
           int pr[2] = {1, 0};
           permute(st, Qt.get(), nc.p(), 2, dims, pr);
-          dgemm(st, false, true, Mp, R, R, 1.0, pv.p(), Mp, Rt.get(), R, 0.0, np_.p(), Mp);
+          gemm_a_ut(st, Mp, R, pv.p(), Mp, Rt.get(), R, np_.p(), Mp);
         }
         cores[k] = std::move(nc);
         cores[k - 1] = std::move(np_);
@@ -276,7 +308,7 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         Core nc = make_core(st, rr, c.I, c.J, c.S);   // C^T Q'^T (rr x N)
         dgemm(st, true, true, rr, N, R, 1.0, tc.C.get(), R, Qt.get(), N, 0.0, nc.p(), rr);
         DBuf<double> T((size_t)R * rr, st);            // R'^T C
-        dgemm(st, true, false, R, rr, R, 1.0, Rt.get(), R, tc.C.get(), R, 0.0, T.get(), R);
+        gemm_ut_b(st, R, rr, Rt.get(), R, tc.C.get(), R, T.get(), R);
         Core np_ = make_core(st, pv.R, pv.I, pv.J, rr);
         dgemm(st, false, false, Mp, rr, R, 1.0, pv.p(), Mp, T.get(), R, 0.0, np_.p(), Mp);
         cores[k] = std::move(nc);
