@@ -88,6 +88,8 @@ struct QrReflectors {
 void householder_qr_keep(cudaStream_t st, int64_t m, int64_t n, double* A, int64_t lda,
                          double* R, int64_t ldr, QrReflectors& f);
 void qr_apply_q(cudaStream_t st, const QrReflectors& f, double* C, int64_t ldc, int64_t ncols);
+// X <- X Q for the nrows x m matrix X (rank-k update per outer block)
+void qr_apply_q_right(cudaStream_t st, const QrReflectors& f, double* X, int64_t ldx, int64_t nrows);
 
 // Thin SVD of a column-major m x n matrix (svd.cu).  Returns all min(m,n)
 // singular values (descending, on the device) and the column-sorted
@@ -127,12 +129,16 @@ double min_sv_lower_bound(cudaStream_t st, int64_t k, const double* U, int64_t l
 // orthonormal basis of the complement of their left (right: right)
 // singular vectors of R'.  false: not resolved inside the iterated block
 // (the caller takes the full SVD).
+// With build_c = false (and t > 0) C is not formed: H = the reflectors f of
+// U_t, C = H [0; I_{k-t}], so X C = (X H)[:, t:] is a rank-t update of X.
 struct TailCut {
   int64_t t = 0;
   DBuf<double> C;
+  QrReflectors f;
+  bool has_c = false;
 };
 bool tail_cut(cudaStream_t st, int64_t k, const double* Rt, int64_t ldr, const double* inv,
-              double delta, bool right, TailCut& out);
+              double delta, bool right, TailCut& out, bool build_c = true);
 
 }  // namespace mpob
 

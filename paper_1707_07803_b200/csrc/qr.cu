@@ -1217,4 +1217,23 @@ void qr_apply_q(cudaStream_t st, const QrReflectors& f, double* C, int64_t ldc, 
   }
 }
 
+// X <- X Q for the nrows x m matrix X: X H_b = X - (X V_b) T_b V_b^T on the
+// columns j0.. of each outer block, first block to last
+void qr_apply_q_right(cudaStream_t st, const QrReflectors& f, double* X, int64_t ldx,
+                      int64_t nrows) {
+  constexpr int NBO = QrReflectors::NBO;
+  const int64_t nob = (int64_t)f.wos.size();
+  if (nrows <= 0 || nob == 0) return;
+  DBuf<double> W((size_t)NBO * nrows, st), W2((size_t)NBO * nrows, st);
+  for (int64_t b = 0; b < nob; ++b) {
+    const int64_t j0 = b * NBO, wo = f.wos[b], mp = f.m - j0;
+    const double* Vo = f.V.get() + f.voff[b];
+    const double* To = f.T.get() + b * NBO * NBO;
+    double* Xb = X + j0 * ldx;
+    dgemm(st, false, false, nrows, wo, mp, 1.0, Xb, ldx, Vo, mp, 0.0, W.get(), nrows);
+    dgemm(st, false, false, nrows, wo, wo, 1.0, W.get(), nrows, To, wo, 0.0, W2.get(), nrows);
+    dgemm(st, false, true, nrows, mp, wo, -1.0, W2.get(), nrows, Vo, mp, 1.0, Xb, ldx);
+  }
+}
+
 }  // namespace mpob

@@ -224,7 +224,7 @@ __global__ void hash_normal_kernel(double* x, int64_t n, uint64_t seed) {
 }
 
 bool tail_cut(cudaStream_t st, int64_t k, const double* Rt, int64_t ldr, const double* inv,
-              double delta, bool right, TailCut& out) {
+              double delta, bool right, TailCut& out, bool build_c) {
   static const bool trace = std::getenv("MPO_B200_TRACE") != nullptr;
   for (int64_t p : {(int64_t)64, (int64_t)256}) {
     if (2 * p > k) break;
@@ -295,7 +295,8 @@ bool tail_cut(cudaStream_t st, int64_t k, const double* Rt, int64_t ldr, const d
     if (!ok) continue;
     out.t = t;
     const int64_t r = k - t;
-    out.C.alloc((size_t)k * r, st);
+    out.has_c = build_c || t == 0;
+    if (out.has_c) out.C.alloc((size_t)k * r, st);
     if (t == 0) {
       set_identity(st, k, k, out.C.get(), k);
       return true;
@@ -305,11 +306,11 @@ bool tail_cut(cudaStream_t st, int64_t k, const double* Rt, int64_t ldr, const d
     DBuf<double> Ut((size_t)k * t, st), Rt_((size_t)t * t, st);
     dgemm(st, false, true, k, t, p, 1.0, X.get(), k, rr.vh.get() + (p - t), p, 0.0, Ut.get(), k);
     // C = H [0; I_r], H the Householder reflectors of U_t
-    QrReflectors f;
-    householder_qr_keep(st, k, t, Ut.get(), k, Rt_.get(), t, f);
+    householder_qr_keep(st, k, t, Ut.get(), k, Rt_.get(), t, out.f);
+    if (!out.has_c) return true;
     fill_zero(st, out.C.get(), k * r);
     set_identity(st, r, r, out.C.get() + t, k);
-    qr_apply_q(st, f, out.C.get(), k, r);
+    qr_apply_q(st, out.f, out.C.get(), k, r);
     return true;
   }
   return false;

@@ -296,7 +296,8 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
       bool cut;
       {
         Trace tr(st, "tail_cut", R, R);
-        cut = tail_on && tail_cut(st, R, Rt.get(), R, inv.get(), delta, false, tc);
+        cut = tail_on && tail_cut(st, R, Rt.get(), R, inv.get(), delta, false, tc,
+                                  /*build_c=*/false);
       }
       if (cut) {
         const int64_t rr = R - tc.t;
@@ -306,11 +307,28 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
           qr_apply_q(st, f, Qt.get(), N, R);
         }
         Core nc = make_core(st, rr, c.I, c.J, c.S);   // C^T Q'^T (rr x N)
-        dgemm(st, true, true, rr, N, R, 1.0, tc.C.get(), R, Qt.get(), N, 0.0, nc.p(), rr);
-        DBuf<double> T((size_t)R * rr, st);            // R'^T C
-        gemm_ut_b(st, R, rr, Rt.get(), R, tc.C.get(), R, T.get(), R);
         Core np_ = make_core(st, pv.R, pv.I, pv.J, rr);
-        dgemm(st, false, false, Mp, rr, R, 1.0, pv.p(), Mp, T.get(), R, 0.0, np_.p(), Mp);
+        if (!tc.has_c) {
+          // C = H_t [0; I_rr] with H_t the t reflectors of the discarded
+          // directions: X C = (X H_t)[:, t:], a rank-t update of X instead of
+          // a product with the dense R x rr matrix C
+          qr_apply_q_right(st, tc.f, Qt.get(), N, N);
+          {
+            int64_t dims[2] = {N, rr};
+            int pr[2] = {1, 0};
+            permute(st, Qt.get() + tc.t * N, nc.p(), 2, dims, pr);
+          }
+          DBuf<double> P1((size_t)Mp * R, st);           // pv R'^T (triangular factor)
+          gemm_a_ut(st, Mp, R, pv.p(), Mp, Rt.get(), R, P1.get(), Mp);
+          qr_apply_q_right(st, tc.f, P1.get(), Mp, Mp);
+          CK(cudaMemcpyAsync(np_.p(), P1.get() + tc.t * Mp, sizeof(double) * Mp * rr,
+                             cudaMemcpyDeviceToDevice, st));
+        } else {
+          dgemm(st, true, true, rr, N, R, 1.0, tc.C.get(), R, Qt.get(), N, 0.0, nc.p(), rr);
+          DBuf<double> T((size_t)R * rr, st);            // R'^T C
+          gemm_ut_b(st, R, rr, Rt.get(), R, tc.C.get(), R, T.get(), R);
+          dgemm(st, false, false, Mp, rr, R, 1.0, pv.p(), Mp, T.get(), R, 0.0, np_.p(), Mp);
+        }
         cores[k] = std::move(nc);
         cores[k - 1] = std::move(np_);
         ++g_round_paths[2];
