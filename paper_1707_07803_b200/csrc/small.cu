@@ -22,7 +22,7 @@ namespace {
 constexpr int S_CT = 512;                // threads (16 warps)
 constexpr int S_W = S_CT / 32;
 constexpr int S_MAXE = 12288;            // doubles of the factored matrix in smem
-constexpr int S_MAXK = 32;               // SVD: k = min(m, n) <= 32 (one warp)
+constexpr int S_MAXK = 64;               // SVD: k = min(m, n) <= 64 (lane = row, two rows per lane above 32)
 constexpr int S_MAXQ = 64;               // QR: kk = min(m, n) <= 64
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -128,10 +128,11 @@ __global__ void __launch_bounds__(S_CT) small_qr_kernel(int m, int n, const doub
   }
 }
 
-// One-sided Jacobi SVD of an m x n matrix, k = min(m, n) <= 32:
+// One-sided Jacobi SVD of an m x n matrix, k = min(m, n) <= 64:
 // QR of the tall orientation (M^T if wide), then cyclic round-robin Jacobi
-// on the k x k factor X (16 warps rotate 16 disjoint column pairs per round,
-// lane = row), converged on chip; then sort and the finishing products.
+// on the k x k factor X (16 warps rotate disjoint column pairs, one or two
+// pairs per warp and round; lane = row, rows lane and lane + 32 when k > 32),
+// converged on chip; then sort and the finishing products.
 __global__ void __launch_bounds__(S_CT) small_svd_kernel(int m, int n, const double* __restrict__ M,
                                                          int64_t ldm, double* __restrict__ s_out,
                                                          double* __restrict__ ucarry,
@@ -140,25 +141,27 @@ __global__ void __launch_bounds__(S_CT) small_svd_kernel(int m, int n, const dou
   extern __shared__ __align__(16) double sm[];
   const bool wide = m <= n;
   const int k = min(m, n), tm = wide ? n : m;
+  const int KP = k <= 32 ? 32 : 64;          // padded order of X and V
   double* A = sm;                            // tm x k: the tall orientation, then reflectors
   double* Cb = A + (size_t)tm * k;           // tm x k: finishing product
-  double* X = Cb + (size_t)tm * k;           // 32 x 32
-  double* V = X + 32 * 32;                   // 32 x 32
-  double* tau = V + 32 * 32;
+  double* X = Cb + (size_t)tm * k;           // KP x KP
+  double* V = X + KP * KP;                   // KP x KP
+  double* tau = V + KP * KP;
   double* red = tau + S_MAXK;
   double* nrm = red + S_W + 1;
-  __shared__ int perm[32];
-  __shared__ int s_rot, s_pair[16][2];
+  __shared__ int perm[S_MAXK];
+  __shared__ int s_rot, s_pair[S_MAXK / 2][2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool two = KP > 32;                  // second row lane + 32
   for (int e = threadIdx.x; e < tm * k; e += S_CT) {
     const int i = e % tm, c = e / tm;   // A[i, c]
     A[e] = wide ? M[c + (int64_t)i * ldm] : M[i + (int64_t)c * ldm];
   }
   __syncthreads();
   block_qr(A, tm, k, tau, red);
-  // X = R^T (wide: M = R^T Q^T) or R (tall: M = Q R), V = I, zero padded to 32
-  for (int e = threadIdx.x; e < 32 * 32; e += S_CT) {
-    const int i = e & 31, c = e >> 5;
+  // X = R^T (wide: M = R^T Q^T) or R (tall: M = Q R), V = I, zero padded to KP
+  for (int e = threadIdx.x; e < KP * KP; e += S_CT) {
+    const int i = e % KP, c = e / KP;
     double v = 0.0;
     if (i < k && c < k) v = wide ? (c <= i ? A[c + (size_t)i * tm] : 0.0)
                                  : (i <= c ? A[i + (size_t)c * tm] : 0.0);
@@ -176,7 +179,10 @@ __global__ void __launch_bounds__(S_CT) small_svd_kernel(int m, int n, const dou
   // rotating forever
   if (warp == 0) {
     double f = 0.0;
-    for (int c = 0; c < k; ++c) f += X[lane + 32 * c] * X[lane + 32 * c];
+    for (int c = 0; c < k; ++c) {
+      f += X[lane + KP * c] * X[lane + KP * c];
+      if (two) f += X[lane + 32 + KP * c] * X[lane + 32 + KP * c];
+    }
     f = warp_sum(f);
     if (lane == 0) red[0] = f;
   }
@@ -196,22 +202,31 @@ __global__ void __launch_bounds__(S_CT) small_svd_kernel(int m, int n, const dou
         s_pair[t][1] = slot(kp - 1 - t);
       }
       __syncthreads();
-      if (warp < kp / 2) {
-        const int p = min(s_pair[warp][0], s_pair[warp][1]);
-        const int q = max(s_pair[warp][0], s_pair[warp][1]);
+      for (int pi = warp; pi < kp / 2; pi += S_W) {
+        const int p = min(s_pair[pi][0], s_pair[pi][1]);
+        const int q = max(s_pair[pi][0], s_pair[pi][1]);
         if (q < k) {
-          const double xp = X[lane + 32 * p], xq = X[lane + 32 * q];
-          const double a = warp_sum(xp * xp), b = warp_sum(xq * xq), c = warp_sum(xp * xq);
+          const double xp = X[lane + KP * p], xq = X[lane + KP * q];
+          const double xp2 = two ? X[lane + 32 + KP * p] : 0.0, xq2 = two ? X[lane + 32 + KP * q] : 0.0;
+          const double a = warp_sum(fma(xp, xp, xp2 * xp2)), b = warp_sum(fma(xq, xq, xq2 * xq2)),
+                       c = warp_sum(fma(xp, xq, xp2 * xq2));
           if (c != 0.0 && fabs(c) > tol * sqrt(a) * sqrt(b) &&
               c * c > floorc * floorc * fro2 * fmax(a, b)) {
             const double zeta = (b - a) / (2.0 * c);
             const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
             const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-            X[lane + 32 * p] = cs * xp - sn * xq;
-            X[lane + 32 * q] = sn * xp + cs * xq;
-            const double vp = V[lane + 32 * p], vq = V[lane + 32 * q];
-            V[lane + 32 * p] = cs * vp - sn * vq;
-            V[lane + 32 * q] = sn * vp + cs * vq;
+            X[lane + KP * p] = cs * xp - sn * xq;
+            X[lane + KP * q] = sn * xp + cs * xq;
+            const double vp = V[lane + KP * p], vq = V[lane + KP * q];
+            V[lane + KP * p] = cs * vp - sn * vq;
+            V[lane + KP * q] = sn * vp + cs * vq;
+            if (two) {
+              X[lane + 32 + KP * p] = cs * xp2 - sn * xq2;
+              X[lane + 32 + KP * q] = sn * xp2 + cs * xq2;
+              const double vp2 = V[lane + 32 + KP * p], vq2 = V[lane + 32 + KP * q];
+              V[lane + 32 + KP * p] = cs * vp2 - sn * vq2;
+              V[lane + 32 + KP * q] = sn * vp2 + cs * vq2;
+            }
             if (lane == 0) s_rot = 1;
           }
         }
@@ -224,21 +239,23 @@ __global__ void __launch_bounds__(S_CT) small_svd_kernel(int m, int n, const dou
   }
   const bool failed = sweep == 60;   // not converged: NaN singular values (the host raises)
   // singular values: column norms, descending, index tie-break
-  if (warp == 0) {
+  if (threadIdx.x < KP) {
+    const int col = threadIdx.x;
     double v = 0.0;
-    for (int i = 0; i < 32; ++i) v += X[i + 32 * lane] * X[i + 32 * lane];
-    v = lane < k ? sqrt(v) : -1.0;
-    nrm[lane] = v;
-    __syncwarp();
+    for (int i = 0; i < KP; ++i) v += X[i + KP * col] * X[i + KP * col];
+    nrm[col] = col < k ? sqrt(v) : -1.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < k) {
+    const int col = threadIdx.x;
+    const double v = nrm[col];
     int rank = 0;
     for (int j = 0; j < k; ++j) {
       const double u = nrm[j];
-      rank += (u > v) || (u == v && j < lane);
+      rank += (u > v) || (u == v && j < col);
     }
-    if (lane < k) {
-      perm[rank] = lane;
-      s_out[rank] = failed ? nan("") : v;
-    }
+    perm[rank] = col;
+    s_out[rank] = failed ? nan("") : v;
   }
   __syncthreads();
   // finishing: wide  M = X Vs^T Q^T ... Ucarry = Ys (k x k), Vh = (Q [Vs; 0])^T
@@ -246,14 +263,14 @@ __global__ void __launch_bounds__(S_CT) small_svd_kernel(int m, int n, const dou
   const double* Fin = wide ? V : X;   // the factor that meets Q
   for (int e = threadIdx.x; e < tm * k; e += S_CT) {
     const int i = e % tm, c = e / tm;
-    Cb[e] = i < k ? Fin[i + 32 * perm[c]] : 0.0;
+    Cb[e] = i < k ? Fin[i + KP * perm[c]] : 0.0;
   }
   __syncthreads();
   block_apply_q(A, tm, k, tau, Cb, tm, k);
   if (wide) {
     for (int e = threadIdx.x; e < k * k; e += S_CT) {
       const int i = e % k, c = e / k;
-      ucarry[i + (int64_t)c * m] = X[i + 32 * perm[c]];
+      ucarry[i + (int64_t)c * m] = X[i + KP * perm[c]];
     }
     for (int e = threadIdx.x; e < k * n; e += S_CT) {
       const int r = e % k, c = e / k;   // vh[r, c] = (Q Vs)[c, r]
@@ -263,7 +280,7 @@ __global__ void __launch_bounds__(S_CT) small_svd_kernel(int m, int n, const dou
     for (int e = threadIdx.x; e < m * k; e += S_CT) ucarry[e] = Cb[e];
     for (int e = threadIdx.x; e < k * k; e += S_CT) {
       const int r = e % k, c = e / k;   // vh[r, c] = Vs[c, r]
-      vh[r + (int64_t)c * k] = V[c + 32 * perm[r]];
+      vh[r + (int64_t)c * k] = V[c + KP * perm[r]];
     }
   }
 }
@@ -274,7 +291,8 @@ size_t qr_smem(int64_t m, int64_t n) {
 }
 size_t svd_smem(int64_t m, int64_t n) {
   const int64_t k = std::min(m, n), tm = std::max(m, n);
-  return sizeof(double) * (size_t)(2 * tm * k + 2 * 32 * 32 + S_MAXK + S_W + 1 + 32);
+  const int64_t kpad = k <= 32 ? 32 : 64;
+  return sizeof(double) * (size_t)(2 * tm * k + 2 * kpad * kpad + S_MAXK + S_W + 1 + S_MAXK);
 }
 
 void set_attrs() {
