@@ -30,6 +30,21 @@ def test_qr_random(shape):
     np.testing.assert_allclose(np.abs(r), np.abs(rl), atol=1e-11 * np.abs(rl).max())
 
 
+@pytest.mark.parametrize("shape", [(257, 257), (1000, 999), (1025, 33), (2047, 129), (4097, 511),
+                                   (8300, 64), (12000, 700), (16385, 130), (20000, 300)])
+def test_qr_odd_shapes(shape):
+    """Shapes off every blocking boundary: partial 32-column panels, partial
+    128-column outer blocks, CTA slices of more than 512 rows (the multi-pass
+    panel paths), panels on either side of the 16384-row limit of the
+    clustered reflector application, narrow (16 / 8 column) cluster panels."""
+    a = np.random.default_rng(sum(shape)).standard_normal(shape)
+    q, r = _qr(a)
+    n = shape[1]
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-13 * np.sqrt(n)
+    assert np.linalg.norm(q @ r - a) <= 1e-13 * np.linalg.norm(a)
+    assert np.abs(np.tril(r, -1)).max() == 0.0
+
+
 def test_qr_rank_deficient_and_graded():
     rng = np.random.default_rng(3)
     a = rng.standard_normal((1500, 200))
