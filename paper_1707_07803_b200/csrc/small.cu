@@ -31,6 +31,46 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// H_j = I - tj v v^T (v = [1; x[j+1:m]]) applied by one warp to the nc <= 4
+// columns Y + c * ldy, c = 0..3, at once: the four dots share the loads of x
+// and reduce in one transposing butterfly (6 exchanges + 4 broadcasts instead
+// of 4 x 5), then the four updates.
+__device__ __forceinline__ void apply_reflector4(const double* x, double tj, int j, int m, double* Y,
+                                                 int ldy, int nc) {
+  const int lane = threadIdx.x & 31;
+  double* y[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) y[u] = Y + (size_t)min(u, nc - 1) * ldy;
+  double w[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) w[u] = lane == 0 ? y[u][j] : 0.0;
+  for (int i = j + 1 + lane; i < m; i += 32) {
+    const double xi = x[i];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = fma(xi, y[u][i], w[u]);
+  }
+  const bool hi = lane & 16, mid = lane & 8;
+  double k0 = (hi ? w[2] : w[0]) + __shfl_xor_sync(0xffffffffu, hi ? w[0] : w[2], 16);
+  double k1 = (hi ? w[3] : w[1]) + __shfl_xor_sync(0xffffffffu, hi ? w[1] : w[3], 16);
+  double k = (mid ? k1 : k0) + __shfl_xor_sync(0xffffffffu, mid ? k0 : k1, 8);
+  k += __shfl_xor_sync(0xffffffffu, k, 4);
+  k += __shfl_xor_sync(0xffffffffu, k, 2);
+  k += __shfl_xor_sync(0xffffffffu, k, 1);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) w[u] = __shfl_sync(0xffffffffu, k, 8 * u) * tj;
+  if (lane == 0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u < nc) y[u][j] -= w[u];
+  }
+  for (int i = j + 1 + lane; i < m; i += 32) {
+    const double xi = x[i];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (u < nc) y[u][i] = fma(-w[u], xi, y[u][i]);
+  }
+}
+
 // In-place Householder QR of the column-major m x n matrix A (ld m) in
 // shared memory, kk = min(m, n) reflectors (dlarfg convention): R in the
 // upper triangle, v_j below the diagonal (v_j[0] = 1 implicit), tau[j].
@@ -65,17 +105,11 @@ __device__ void block_qr(double* A, int m, int n, double* tau, double* red) {
     if (tau[j] != 0.0)
       for (int i = j + 1 + threadIdx.x; i < m; i += S_CT) x[i] *= scale;
     __syncthreads();
-    // apply H_j to the trailing columns, one warp per column
+    // apply H_j to the trailing columns, four columns per warp
     const double tj = tau[j];
     if (tj != 0.0) {
-      for (int c = j + 1 + warp; c < n; c += S_W) {
-        double* y = A + (size_t)c * m;
-        double w = lane == 0 ? y[j] : 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) w += x[i] * y[i];
-        w = warp_sum(w) * tj;
-        if (lane == 0) y[j] -= w;
-        for (int i = j + 1 + lane; i < m; i += 32) y[i] -= w * x[i];
-      }
+      for (int c = j + 1 + 4 * warp; c < n; c += 4 * S_W)
+        apply_reflector4(x, tj, j, m, A + (size_t)c * m, m, min(4, n - c));
     }
     __syncthreads();
   }
@@ -85,19 +119,13 @@ __device__ void block_qr(double* A, int m, int n, double* tau, double* red) {
 // zero on entry: the reflectors of block_qr applied backwards (dorgqr).
 __device__ void block_apply_q(const double* A, int m, int kk, const double* tau, double* C,
                               int ldc, int nc) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5;
   for (int j = kk - 1; j >= 0; --j) {
     const double tj = tau[j];
     if (tj != 0.0) {
       const double* x = A + (size_t)j * m;
-      for (int c = warp; c < nc; c += S_W) {
-        double* y = C + (size_t)c * ldc;
-        double w = lane == 0 ? y[j] : 0.0;
-        for (int i = j + 1 + lane; i < m; i += 32) w += x[i] * y[i];
-        w = warp_sum(w) * tj;
-        if (lane == 0) y[j] -= w;
-        for (int i = j + 1 + lane; i < m; i += 32) y[i] -= w * x[i];
-      }
+      for (int c = 4 * warp; c < nc; c += 4 * S_W)
+        apply_reflector4(x, tj, j, m, C + (size_t)c * ldc, ldc, min(4, nc - c));
     }
     __syncthreads();
   }
