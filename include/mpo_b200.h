@@ -47,7 +47,8 @@ unsigned long long mpo_b200_launch_count(void); /* kernels launched so far */
 int mpo_b200_round_paths(unsigned long long* out);
 /* CUDA-event timing per kernel family (bench roofline): which = 0
  * jacobi_gram, 1 jacobi_eig, 2 jacobi_apply, 3 dgemm (incl. split-K
- * reduction), 4 QR panel; enable(1) resets.  Timed launches synchronise
+ * reduction), 4 QR panel, 5 QR panel-reflector application (in-block and
+ * look-ahead updates); enable(1) resets.  Timed launches synchronise
  * (profiling runs only). */
 int mpo_b200_profile_enable(int on);
 int mpo_b200_profile_read(int which, double* ms, double* flops, unsigned long long* launches);
