@@ -294,18 +294,26 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
       // smallest singular values alone; M_r = (R'^T C)(Q' C)^T
       TailCut tc;
       bool cut;
+      if (square && tail_on) {
+        // the certificate failed: the tail truncation will need Q' = H [I; 0];
+        // it forms on the Q stream while tail_cut iterates on this one
+        SideStream& sd = side_stream(st);
+        Qt.alloc((size_t)N * R, st);
+        CK(cudaEventRecord(sd.eqf, st));
+        CK(cudaStreamWaitEvent(sd.qs, sd.eqf, 0));
+        set_identity(sd.qs, N, R, Qt.get(), N);
+        qr_apply_q(sd.qs, f, Qt.get(), N, R);
+        CK(cudaEventRecord(sd.eq, sd.qs));
+        sd.q_pending = true;
+      }
       {
         Trace tr(st, "tail_cut", R, R);
         cut = tail_on && tail_cut(st, R, Rt.get(), R, inv.get(), delta, false, tc,
                                   /*build_c=*/false);
       }
+      join_deferred_q(st);
       if (cut) {
         const int64_t rr = R - tc.t;
-        if (square) {   // Q' from its reflectors: Q' = H [I; 0]
-          Qt.alloc((size_t)N * R, st);
-          set_identity(st, N, R, Qt.get(), N);
-          qr_apply_q(st, f, Qt.get(), N, R);
-        }
         Core nc = make_core(st, rr, c.I, c.J, c.S);   // C^T Q'^T (rr x N)
         Core np_ = make_core(st, pv.R, pv.I, pv.J, rr);
         if (!tc.has_c) {
