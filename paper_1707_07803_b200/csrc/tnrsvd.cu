@@ -237,6 +237,7 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
       // below), its reflectors are kept instead
       const bool square = R == N;
       DBuf<double> At((size_t)N * R, st), Qt, Rt((size_t)R * R, st);
+      DBuf<double> P1;   // pv R'^T (Mp x R) for the tail truncation
       QrReflectors f;
       DeferredQScope qscope(st);   // joined before Qt is released, also when unwinding
       {
@@ -294,15 +295,20 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
       // smallest singular values alone; M_r = (R'^T C)(Q' C)^T
       TailCut tc;
       bool cut;
-      if (square && tail_on) {
-        // the certificate failed: the tail truncation will need Q' = H [I; 0];
-        // it forms on the Q stream while tail_cut iterates on this one
+      if (tail_on) {
+        // the certificate failed: the tail truncation will need Q' (= H [I; 0]
+        // for a square bond, from the LQ's reflectors) and pv R'^T; they form
+        // on the Q stream while tail_cut iterates on this one
         SideStream& sd = side_stream(st);
-        Qt.alloc((size_t)N * R, st);
+        if (square) Qt.alloc((size_t)N * R, st);
+        P1.alloc((size_t)Mp * R, st);
         CK(cudaEventRecord(sd.eqf, st));
         CK(cudaStreamWaitEvent(sd.qs, sd.eqf, 0));
-        set_identity(sd.qs, N, R, Qt.get(), N);
-        qr_apply_q(sd.qs, f, Qt.get(), N, R);
+        if (square) {
+          set_identity(sd.qs, N, R, Qt.get(), N);
+          qr_apply_q(sd.qs, f, Qt.get(), N, R);
+        }
+        gemm_a_ut(sd.qs, Mp, R, pv.p(), Mp, Rt.get(), R, P1.get(), Mp);
         CK(cudaEventRecord(sd.eq, sd.qs));
         sd.q_pending = true;
       }
@@ -326,8 +332,6 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
             int pr[2] = {1, 0};
             permute(st, Qt.get() + tc.t * N, nc.p(), 2, dims, pr);
           }
-          DBuf<double> P1((size_t)Mp * R, st);           // pv R'^T (triangular factor)
-          gemm_a_ut(st, Mp, R, pv.p(), Mp, Rt.get(), R, P1.get(), Mp);
           qr_apply_q_right(st, tc.f, P1.get(), Mp, Mp);
           CK(cudaMemcpyAsync(np_.p(), P1.get() + tc.t * Mp, sizeof(double) * Mp * rr,
                              cudaMemcpyDeviceToDevice, st));
