@@ -248,9 +248,18 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         if (square) {
           householder_qr_keep(st, N, R, At.get(), N, Rt.get(), R, f);
         } else {
-          // Q' forms on the Q stream while the certificate below runs
+          // Q' forms on the Q stream while the certificate below runs, and
+          // behind it pv R'^T: the left neighbour's new unfolding if the bond
+          // is certified, the tail truncation's P1 if not
           Qt.alloc((size_t)N * R, st);
+          P1.alloc((size_t)Mp * R, st);
           householder_qr(st, N, R, At.get(), N, Qt.get(), N, Rt.get(), R, /*defer_q=*/true);
+          SideStream& sd = side_stream(st);
+          CK(cudaEventRecord(sd.eqf, st));
+          CK(cudaStreamWaitEvent(sd.qs, sd.eqf, 0));
+          gemm_a_ut(sd.qs, Mp, R, pv.p(), Mp, Rt.get(), R, P1.get(), Mp);
+          CK(cudaEventRecord(sd.eq, sd.qs));
+          sd.q_pending = true;
         }
       }
       double lb;
@@ -274,9 +283,11 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
       join_deferred_q(st);
       if (lb > cert_margin * delta) {
         Core nc = make_core(st, R, c.I, c.J, c.S);
-        Core np_ = make_core(st, pv.R, pv.I, pv.J, R);
+        Core np_;
+        np_.R = pv.R; np_.I = pv.I; np_.J = pv.J; np_.S = R;
         if (square) {
           // core k <- I (orthogonal), core k-1 absorbs M itself
+          np_ = make_core(st, pv.R, pv.I, pv.J, R);
           set_identity(st, N, N, nc.p(), N);
           dgemm(st, false, false, Mp, N, R, 1.0, pv.p(), Mp, c.p(), R, 0.0, np_.p(), Mp);
         } else {
@@ -284,7 +295,7 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
           int64_t dims[2] = {N, R};
           int pr[2] = {1, 0};
           permute(st, Qt.get(), nc.p(), 2, dims, pr);
-          gemm_a_ut(st, Mp, R, pv.p(), Mp, Rt.get(), R, np_.p(), Mp);
+          np_.buf = std::move(P1);
         }
         cores[k] = std::move(nc);
         cores[k - 1] = std::move(np_);
@@ -300,17 +311,17 @@ void truncate_r2l(cudaStream_t st, Cores& cores, double tol) {
         // for a square bond, from the LQ's reflectors) and pv R'^T; they form
         // on the Q stream while tail_cut iterates on this one
         SideStream& sd = side_stream(st);
-        if (square) Qt.alloc((size_t)N * R, st);
-        P1.alloc((size_t)Mp * R, st);
-        CK(cudaEventRecord(sd.eqf, st));
-        CK(cudaStreamWaitEvent(sd.qs, sd.eqf, 0));
         if (square) {
+          Qt.alloc((size_t)N * R, st);
+          P1.alloc((size_t)Mp * R, st);
+          CK(cudaEventRecord(sd.eqf, st));
+          CK(cudaStreamWaitEvent(sd.qs, sd.eqf, 0));
           set_identity(sd.qs, N, R, Qt.get(), N);
           qr_apply_q(sd.qs, f, Qt.get(), N, R);
+          gemm_a_ut(sd.qs, Mp, R, pv.p(), Mp, Rt.get(), R, P1.get(), Mp);
+          CK(cudaEventRecord(sd.eq, sd.qs));
+          sd.q_pending = true;
         }
-        gemm_a_ut(sd.qs, Mp, R, pv.p(), Mp, Rt.get(), R, P1.get(), Mp);
-        CK(cudaEventRecord(sd.eq, sd.qs));
-        sd.q_pending = true;
       }
       {
         Trace tr(st, "tail_cut", R, R);
