@@ -105,11 +105,13 @@ __device__ void block_qr(double* A, int m, int n, double* tau, double* red) {
     if (tau[j] != 0.0)
       for (int i = j + 1 + threadIdx.x; i < m; i += S_CT) x[i] *= scale;
     __syncthreads();
-    // apply H_j to the trailing columns, four columns per warp
+    // apply H_j to the trailing columns: four columns per warp, or one per
+    // warp when there is a warp for every column
     const double tj = tau[j];
     if (tj != 0.0) {
-      for (int c = j + 1 + 4 * warp; c < n; c += 4 * S_W)
-        apply_reflector4(x, tj, j, m, A + (size_t)c * m, m, min(4, n - c));
+      const int per = n - j - 1 <= S_W ? 1 : 4;
+      for (int c = j + 1 + per * warp; c < n; c += per * S_W)
+        apply_reflector4(x, tj, j, m, A + (size_t)c * m, m, min(per, n - c));
     }
     __syncthreads();
   }
@@ -124,8 +126,9 @@ __device__ void block_apply_q(const double* A, int m, int kk, const double* tau,
     const double tj = tau[j];
     if (tj != 0.0) {
       const double* x = A + (size_t)j * m;
-      for (int c = 4 * warp; c < nc; c += 4 * S_W)
-        apply_reflector4(x, tj, j, m, C + (size_t)c * ldc, ldc, min(4, nc - c));
+      const int per = nc <= S_W ? 1 : 4;
+      for (int c = per * warp; c < nc; c += per * S_W)
+        apply_reflector4(x, tj, j, m, C + (size_t)c * ldc, ldc, min(per, nc - c));
     }
     __syncthreads();
   }
